@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the fixpoint min-relaxation hot path (SSSP / BFS / CC).
+
+One STEP = one pass of the whole hot path over the workload graph: every
+algorithm (SSSP, BFS, CC) in every processing style (VERTEX, EDGE, WORKLIST)
+through the C ABI, i.e. 9 library calls, each doing init -> device-side
+fixpoint loop -> output (graph residency a1 is
+outside the timed region except in the e2e number).
+
+Metric (BASELINE.json): GTEPS = sum over the step's runs of m_counted / time,
+m_counted = arcs whose source is reached (SSSP/BFS; Graph500-style, DESIGN.md
+R13) or m (CC).  value is the whole-job aggregate over all ranks.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config rand-25M]
+        python bench.py --impl reference ...   (the CPU oracle, timed on host cores)
+Multi-GPU (N>1, torchrun): "parallel sections" replica mode of PAPER.md:1587-1597
+-- every rank runs the step on its own seeded instance (weak scaling); there is
+no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGOS = ("sssp", "bfs", "cc")
+STYLES = ("vertex", "edge", "worklist")
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="rand-25M")
+    ap.add_argument("--algos", default=",".join(ALGOS))
+    ap.add_argument("--styles", default=",".join(STYLES))
+    ap.add_argument("--impl", default="falcon", choices=["falcon", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-max-steps", type=int, default=3)
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def m_counted(G, algo, out) -> int:
+    """Arcs whose source ends with a finite value (SSSP/BFS); m for CC."""
+    if algo == "cc":
+        return int(G.m)
+    deg = np.diff(G.row_off.astype(np.int64))
+    return int(deg[np.asarray(out) != 2147483647].sum())
+
+
+def algorithmic_bytes(algo, style, st, n, m) -> int:
+    """Bytes the relax kernel must move for the work it did:
+    per processed vertex 8 (row_off amortised 4 + own value 4) [+4 frontier
+    read, WORKLIST]; per relaxed arc 12 (SSSP: col, w, gathered value) or 8
+    (BFS/CC: col, gathered value); per successful update 4 [+4 append];
+    VERTEX scans one activity word per vertex per round; EDGE streams src[]
+    (4 B per arc per round) and gathers the source value (4 B per active arc)."""
+    per_arc = 12 if algo == "sssp" else 8
+    V, E, U, R = st["vertices_processed"], st["edges_relaxed"], st["updates"], st["iterations"]
+    b = E * per_arc + U * 4
+    if style == "vertex":
+        b += V * 8 + R * 4 * n
+    elif style == "edge":
+        b += R * 4 * m + E * 4
+    else:
+        b += V * 12 + U * 4
+    return int(b)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch for the dominant kernel, from the
+    committed ncu --set full summary (profiles/ncu_traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(kernel_key)
+    return None if v is None else float(v.get("dram_bytes_per_launch"))
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_pass(G, algos):
+    """One oracle pass (each algorithm once, concurrently in threads: ctypes
+    releases the GIL).  Returns (m_counted total, wall seconds, threads)."""
+    import oracle
+    res = {}
+
+    def one(a):
+        res[a] = oracle.run(a, G)
+
+    ths = [threading.Thread(target=one, args=(a,)) for a in algos]
+    t0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    return sum(m_counted(G, a, res[a]) for a in algos), dt, len(algos)
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle, as it stands, on the host cores."""
+    import graphgen as gg
+    if rank != 0:
+        return
+    algos = [a for a in args.algos.split(",") if a]
+    G = gg.config(args.config)
+    tiny = gg.config("tiny")
+    for _ in range(args.warmup):          # warm-up on the tiny config (page-in, caches)
+        oracle_pass(tiny, algos)
+    steps = max(1, min(args.steps, args.ref_max_steps))
+    tot_m, tot_t, cores = 0, 0.0, len(algos)
+    for _ in range(steps):
+        mc, dt, cores = oracle_pass(G, algos)
+        tot_m += mc
+        tot_t += dt
+    value = tot_m / tot_t / 1e9
+    sample = (f"{steps} step(s) of one oracle pass ({'+'.join(algos)}, one algorithm per host thread) over "
+              f"{args.config}; warm-up on 'tiny'")
+    line = {"impl": "reference", "metric": "SSSP/BFS/CC GTEPS (aggregate over runs per step)", "value": value,
+            "unit": "GTEPS", "n_gpus": world, "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic",
+            "config": {"workload": args.config, "n": G.n, "m": G.m, "algos": algos, "styles": ["oracle"]},
+            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line, args)
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(s + "\n")
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import graphgen as gg
+    import paper_1903_01665_b200 as fb
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fb.load()
+    algos = [a for a in args.algos.split(",") if a]
+    styles = [s for s in args.styles.split(",") if s]
+
+    # Workload: the BASELINE.json config; replica r uses seed + r (weak scaling).
+    if world > 1 and rank > 0:
+        base = gg.CONFIGS[args.config]
+        G = {"rand-25M": lambda: gg.er(25_000_000, 100_000_000, 25 + rank, name="rand-25M"),
+             "rmat-10M": lambda: gg.rmat(10_000_000, 100_000_000, 10 + rank, name="rmat-10M"),
+             "grid-24M": lambda: gg.grid(6000, 4000, 24 + rank, name="grid-24M")}.get(args.config, base)()
+    else:
+        G = gg.config(args.config)
+    stream = torch.cuda.current_stream()
+    g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream, flags=fb.LOAD_BUILD_COO)
+    out = torch.empty(G.n, dtype=torch.int32, device="cuda")
+    runs = [(a, s) for a in algos for s in styles]
+
+    def step(collect=None):
+        launches = 0
+        for a, s in runs:
+            st = fb.run(g, a, s, out, G.source)
+            launches += st.kernel_launches
+            if collect is not None:
+                collect.setdefault((a, s), []).append(st.as_dict())
+        return launches
+
+    # m_counted per run (outputs are unique fixpoints: style-independent)
+    mc = {}
+    for a in algos:
+        fb.run(g, a, styles[0], out, G.source)
+        mc[a] = m_counted(G, a, out.cpu().numpy())
+    units_per_step = sum(mc[a] for a, _ in runs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    per_run = {}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        launches = 0
+        for _ in range(args.steps):
+            launches += step(per_run)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * units_per_step * args.steps / (ms_total * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel: one profiled step (host-driven loop,
+    # CUDA events around every relax launch on the library stream)
+    fb.falcon_set_profiling(g, True)
+    prof = {}
+    step(prof)
+    fb.falcon_set_profiling(g, False)
+    hbm, hbm_src = peaks()
+    shares = {k: v[0]["relax_ms"] for k, v in prof.items()}
+    dom = max(shares, key=shares.get)
+    dst = prof[dom][0]
+    bytes_dom = algorithmic_bytes(dom[0], dom[1], dst, G.n, G.m)
+    achieved = bytes_dom / (dst["relax_ms"] * 1e-3) / 1e9
+    key = f"{dom[0]}/{dom[1]}"
+    traffic = ncu_traffic(key)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "kernel": f"relax {key}", "peak_source": hbm_src,
+                "relax_ms": dst["relax_ms"], "relax_launches": dst["relax_launches"],
+                "algorithmic_bytes": bytes_dom, "share_of_step": dst["relax_ms"] / ms_step}
+
+    breakdown = {}
+    for (a, s), lst in per_run.items():
+        ms = statistics.median(x["ms"] for x in lst)
+        x = lst[-1]
+        p = prof.get((a, s), [x])[0]
+        bts = algorithmic_bytes(a, s, x, G.n, G.m)
+        breakdown[f"{a}/{s}"] = {"ms": ms, "gteps": mc[a] / (ms * 1e-3) / 1e9, "iterations": x["iterations"],
+                                 "edges_relaxed": x["edges_relaxed"], "updates": x["updates"],
+                                 "relax_ms": p["relax_ms"], "alg_GBps_relax": bts / (p["relax_ms"] * 1e-3) / 1e9
+                                 if p["relax_ms"] > 0 else None,
+                                 "one_pass_eff": ((12 if a == "sssp" else 8) * G.m + 8 * G.n) / (ms * 1e-3) / 1e9 / hbm}
+
+    # ---- e2e through the C ABI with HOST buffers (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(a).pin_memory()
+        h_ro, h_col, h_w = pin(G.row_off), pin(G.col), pin(G.w)
+        h_out = torch.empty(G.n, dtype=torch.int32).pin_memory()
+        e_steps = max(1, min(args.steps, 3))
+
+        def e2e_step():
+            gh = fb.graph_load_csr(G.n, G.m, h_ro, h_col, h_w, device=local, stream=stream)
+            for a, s in runs:
+                fb.run(gh, a, s, h_out, G.source)
+            fb.graph_free(gh)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",
+               "h2d_bytes_per_step": 4 * (G.n + 1) + 8 * G.m, "d2h_bytes_per_step": 4 * G.n * len(runs),
+               "steps": e_steps, "ms_per_step": ems / e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tot, dt, cores = oracle_pass(G, algos)
+        cpu = {"value": tot / dt / 1e9, "unit": "GTEPS", "cores": cores, "kind": "oracle",
+               "sample": f"one oracle pass ({'+'.join(algos)}, one algorithm per host thread, single-threaded "
+                         f"each) over {args.config}: {dt:.1f} s wall; host has {os.cpu_count()} cores"}
+
+    if rank == 0:
+        line = {"metric": "SSSP/BFS/CC GTEPS (aggregate over runs per step)", "value": value, "unit": "GTEPS",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic",
+                "config": {"workload": args.config, "n": G.n, "m": G.m, "source": G.source, "algos": algos,
+                           "styles": styles, "runs_per_step": len(runs),
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "inputs larger than L2 (CSR+COO %.2f GB vs 126 MB L2); each run re-initialises "
+                                 "its value array" % ((4 * (G.n + 1) + 12 * G.m) / 1e9)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "per_run": breakdown}
+        emit(line, args)
+    fb.graph_free(g)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

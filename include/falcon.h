@@ -1,0 +1,147 @@
+/*
+ * falcon.h -- C ABI of the B200-native fixpoint min-relaxation library
+ * (SSSP / BFS / connected components) after arXiv 1903.01665 ("adaptive
+ * Falcon").  Plain C types only: no torch, no CUDA types in the signatures
+ * (streams are passed as void*).
+ *
+ * The operation (Alg. "SSSP: iterating over Points in
+ * Falcon", Alg. "SSSP: iterating over Edges";
+ * PAPER.md:1727-1730 §2): starting from dist[source] = 0 and dist = MAX_INT
+ * elsewhere, apply  MIN(t.dist, p.dist + weight(p->t), changed)  to arcs p->t
+ * until no value changes.  BFS is the level-synchronous variant of
+ * PAPER.md:1302-1329 (Alg. "BFS Algorithm in Falcon for CPU"); CC is the
+ * "propagation based" component labelling named at PAPER.md:7, 73.
+ *
+ * The three processing styles are the paper's vertex-based, edge-based and
+ * worklist-based codes (§3.1, 1567-1571 §3.3), selected at
+ * run time instead of compile time.  All styles return
+ * bit-identical results: each output is the unique least fixpoint.
+ *
+ * Common conventions
+ *  - Every call is synchronous: it returns with its outputs complete.  Work is
+ *    issued on the stream given at load time (falcon_load_opts_t.cuda_stream,
+ *    a cudaStream_t passed as void*), or on a stream the graph owns.
+ *  - Pointers marked (host|device) may be either; the library detects which
+ *    with cudaPointerGetAttributes and copies accordingly.  Inputs are only
+ *    borrowed for the duration of the call.  Outputs are caller-allocated.
+ *  - Errors are returned as falcon_status_t, never thrown; a thread-local
+ *    message is available from falcon_last_error().  After a non-OK status the
+ *    outputs are unspecified; the graph stays usable except after
+ *    FALCON_ERR_CUDA.
+ *  - Not thread-safe per graph: do not call two algorithms on the same
+ *    falcon_graph_t concurrently (they share the graph's scratch buffers).
+ */
+#ifndef FALCON_H
+#define FALCON_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FALCON_API __attribute__((visibility("default")))
+#else
+#define FALCON_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* INF = MAX_INT of PAPER.md:1679 (SSSP) / the BFS "infinity" of PAPER.md:1318,
+ * unified as INT32_MAX.  Unreachable vertices report it. */
+#define FALCON_INF 2147483647
+
+typedef enum {
+    FALCON_STYLE_VERTEX = 0,   /* topology-driven over CSR rows   */
+    FALCON_STYLE_EDGE = 1,     /* topology-driven over COO arcs   */
+    FALCON_STYLE_WORKLIST = 2  /* data-driven over a frontier queue */
+} falcon_style_t;
+
+typedef enum {
+    FALCON_OK = 0,
+    FALCON_ERR_INVALID_ARG = 1,   /* NULL pointer, n < 1, n >= 2^31, m >= 2^32, bad style      */
+    FALCON_ERR_OUT_OF_RANGE = 2,  /* row_off not 0..m nondecreasing, col >= n, w < 0, src >= n */
+    FALCON_ERR_NO_MEMORY = 3,     /* device allocation failed                                  */
+    FALCON_ERR_CUDA = 4,          /* any other CUDA runtime error (graph may be unusable)      */
+    FALCON_ERR_OVERFLOW = 5,      /* a finite distance would reach FALCON_INF                  */
+    FALCON_ERR_NOT_CONVERGED = 6, /* iteration cap (n + 2 rounds) exceeded                     */
+    FALCON_ERR_COMM = 7,          /* reserved: multi-GPU communication failure                 */
+    FALCON_ERR_UNSUPPORTED = 8    /* option not supported by this build                        */
+} falcon_status_t;
+
+typedef struct falcon_graph falcon_graph_t; /* opaque; owns its device memory */
+
+/* graph_load_csr options (pass NULL for defaults). */
+#define FALCON_LOAD_BUILD_COO 0x1u  /* build the COO src[] array now (else lazily on first EDGE call) */
+
+typedef struct {
+    int device;          /* CUDA device ordinal; -1 = current device                 */
+    void *cuda_stream;   /* cudaStream_t to issue work on; NULL = a stream owned by the graph */
+    uint32_t flags;      /* FALCON_LOAD_* bits                                       */
+} falcon_load_opts_t;
+
+/* Per-call statistics (all counters are device-side totals for the call). */
+typedef struct {
+    int64_t iterations;         /* fixpoint rounds executed (BFS: levels + 1)              */
+    int64_t vertices_processed; /* active vertices / frontier items expanded                */
+    int64_t edges_relaxed;      /* arcs on which MIN was evaluated                          */
+    int64_t updates;            /* successful MIN updates (value strictly decreased)        */
+    int64_t kernel_launches;    /* library kernels launched for the call                   */
+    double ms;                  /* device time from init to result (CUDA events), excl. D2H */
+    double relax_ms;            /* profiling mode only: summed relax-kernel time, else -1  */
+    int64_t relax_launches;     /* profiling mode only: relax-kernel launches, else 0      */
+} falcon_stats_t;
+
+/* Load a graph in CSR form (§3.1: CSR for vertex-based,
+ * an edge list for edge-based code; SPEC.md:408-413 GraphStore invariants).
+ *   n        vertices, 1 <= n < 2^31
+ *   m        arcs, 0 <= m < 2^32
+ *   row_off  (host|device) uint32[n+1]: row_off[0]==0, nondecreasing, row_off[n]==m
+ *   col      (host|device) uint32[m]: arc targets, each < n
+ *   w        (host|device) int32[m] arc weights >= 0, or NULL = every weight 1
+ *   opts     NULL or options above
+ *   out      receives the new graph handle (owned by the caller; free with graph_free)
+ * Copies everything into library-owned, 16-byte aligned device arrays.
+ * Errors: INVALID_ARG, OUT_OF_RANGE (validated on the device), NO_MEMORY, CUDA. */
+FALCON_API falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col,
+                               const int32_t *w, const falcon_load_opts_t *opts, falcon_graph_t **out);
+
+/* Release all device memory of the graph.  NULL is a no-op. */
+FALCON_API falcon_status_t graph_free(falcon_graph_t *g);
+
+/* Query vertex / arc counts of a loaded graph. */
+FALCON_API falcon_status_t graph_info(const falcon_graph_t *g, int64_t *n, int64_t *m);
+
+/* Single-source shortest paths: dist_out[v] = min over directed paths
+ * source ~> v of the sum of weights, FALCON_INF if unreachable
+ * (PAPER.md:1727-1730).  dist_out: (host|device) int32[n].  stats: nullable.
+ * Errors: INVALID_ARG (source >= n, bad style), OVERFLOW, NOT_CONVERGED, CUDA. */
+FALCON_API falcon_status_t falcon_sssp(falcon_graph_t *g, uint32_t source, falcon_style_t style, int32_t *dist_out,
+                            falcon_stats_t *stats);
+
+/* Breadth-first levels: level_out[v] = fewest arcs on a directed path
+ * source ~> v, FALCON_INF if unreachable.  Weights are
+ * ignored.  level_out: (host|device) int32[n]. */
+FALCON_API falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon_style_t style, int32_t *level_out,
+                           falcon_stats_t *stats);
+
+/* Connected components of the undirected view (weak components): label_out[v]
+ * = smallest vertex id in v's component (min-label convention
+ * SPEC.md:452).  Weights and arc direction are ignored.
+ * label_out: (host|device) int32[n]. */
+FALCON_API falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats);
+
+/* Profiling mode (off by default): when on, the fixpoint loop is driven from
+ * the host and every relax-kernel launch is bracketed by CUDA events, filling
+ * falcon_stats_t.relax_ms / relax_launches.  Results are identical. */
+FALCON_API falcon_status_t falcon_set_profiling(falcon_graph_t *g, int enable);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+FALCON_API const char *falcon_last_error(void);
+
+/* Library version string. */
+FALCON_API const char *falcon_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FALCON_H */

@@ -1,0 +1,205 @@
+"""Thin Python binding of the C ABI in include/falcon.h (libfalcon.so).
+
+Argument marshalling only: every step of the path runs in the library's
+sm_100a kernels.  There is no CPU fallback -- if libfalcon.so cannot be loaded
+every call raises.  Arrays may be numpy arrays (host) or torch tensors (host
+or CUDA); PyTorch is used only for device memory and streams.
+
+Names follow the C ABI: graph_load_csr, graph_free, graph_info, falcon_sssp,
+falcon_bfs, falcon_cc, falcon_set_profiling, falcon_last_error, falcon_version.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "falcon_sssp", "falcon_bfs", "falcon_cc",
+           "falcon_set_profiling", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
+           "STYLES", "INF", "LIB_PATH"]
+
+INF = 2147483647
+STYLE_VERTEX, STYLE_EDGE, STYLE_WORKLIST = 0, 1, 2
+STYLES = {"vertex": STYLE_VERTEX, "edge": STYLE_EDGE, "worklist": STYLE_WORKLIST}
+LOAD_BUILD_COO = 0x1
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "NO_MEMORY", 4: "CUDA", 5: "OVERFLOW",
+          6: "NOT_CONVERGED", 7: "COMM", 8: "UNSUPPORTED"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfalcon.so")
+_lib = None
+
+
+class FalconError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class FalconStats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("vertices_processed", ctypes.c_int64),
+                ("edges_relaxed", ctypes.c_int64), ("updates", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("ms", ctypes.c_double),
+                ("relax_ms", ctypes.c_double), ("relax_launches", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class _LoadOpts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint32)]
+
+
+def load(build_if_missing: bool = False):
+    """Load libfalcon.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        if not build_if_missing:
+            raise FalconError(4, f"{LIB_PATH} not built: run __graft_entry__.build() "
+                                 "(there is no CPU fallback)")
+        from . import _build
+        _build.build()
+    lib = ctypes.CDLL(LIB_PATH)
+    p, i64, u32, st = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int
+    lib.graph_load_csr.argtypes = [i64, i64, p, p, p, ctypes.POINTER(_LoadOpts), ctypes.POINTER(p)]
+    lib.graph_free.argtypes = [p]
+    lib.graph_info.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.falcon_sssp.argtypes = [p, u32, ctypes.c_int, p, ctypes.POINTER(FalconStats)]
+    lib.falcon_bfs.argtypes = [p, u32, ctypes.c_int, p, ctypes.POINTER(FalconStats)]
+    lib.falcon_cc.argtypes = [p, ctypes.c_int, p, ctypes.POINTER(FalconStats)]
+    lib.falcon_set_profiling.argtypes = [p, ctypes.c_int]
+    for f in (lib.graph_load_csr, lib.graph_free, lib.graph_info, lib.falcon_sssp, lib.falcon_bfs, lib.falcon_cc,
+              lib.falcon_set_profiling):
+        f.restype = st
+    lib.falcon_last_error.restype = ctypes.c_char_p
+    lib.falcon_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):  # torch tensor (host or CUDA)
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    if hasattr(x, "ctypes"):  # numpy
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(x.ctypes.data)
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FalconError(rc, (load().falcon_last_error() or b"").decode())
+
+
+def _style(style) -> int:
+    if isinstance(style, str):
+        return STYLES[style.lower()]
+    return int(style)
+
+
+def _check_dtype(x, kind: str, name: str):
+    dt = getattr(x, "dtype", None)
+    if dt is None:
+        return
+    s = str(dt)
+    ok = {"u32": ("uint32",), "i32": ("int32",)}[kind]
+    if not any(s.endswith(o) for o in ok):
+        raise TypeError(f"{name} must be {ok[0]}, got {s}")
+
+
+class Graph:
+    """Owning handle of a falcon_graph_t (freed by graph_free or on GC)."""
+
+    def __init__(self, handle: ctypes.c_void_p, n: int, m: int):
+        self.handle = handle
+        self.n = n
+        self.m = m
+
+    def __del__(self):
+        try:
+            graph_free(self)
+        except Exception:
+            pass
+
+    @property
+    def _as_parameter_(self):
+        return self.handle
+
+
+def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, stream=None, flags: int = 0) -> Graph:
+    """graph_load_csr(n, m, row_off u32[n+1], col u32[m], w i32[m] | None, ...)."""
+    lib = load()
+    _check_dtype(row_off, "u32", "row_off"); _check_dtype(col, "u32", "col")
+    if w is not None:
+        _check_dtype(w, "i32", "w")
+    if stream is not None and hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    opts = _LoadOpts(device, ctypes.c_void_p(stream) if stream else None, flags)
+    out = ctypes.c_void_p()
+    _check(lib.graph_load_csr(n, m, _ptr(row_off), _ptr(col), _ptr(w), ctypes.byref(opts), ctypes.byref(out)))
+    return Graph(out, n, m)
+
+
+def graph_free(g: Graph):
+    if g is not None and g.handle:
+        load().graph_free(g.handle)
+        g.handle = None
+
+
+def graph_info(g: Graph):
+    n, m = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().graph_info(g.handle, ctypes.byref(n), ctypes.byref(m)))
+    return n.value, m.value
+
+
+def falcon_sssp(g: Graph, source: int, style, dist_out) -> FalconStats:
+    st = FalconStats()
+    _check_dtype(dist_out, "i32", "dist_out")
+    _check(load().falcon_sssp(g.handle, source, _style(style), _ptr(dist_out), ctypes.byref(st)))
+    return st
+
+
+def falcon_bfs(g: Graph, source: int, style, level_out) -> FalconStats:
+    st = FalconStats()
+    _check_dtype(level_out, "i32", "level_out")
+    _check(load().falcon_bfs(g.handle, source, _style(style), _ptr(level_out), ctypes.byref(st)))
+    return st
+
+
+def falcon_cc(g: Graph, style, label_out) -> FalconStats:
+    st = FalconStats()
+    _check_dtype(label_out, "i32", "label_out")
+    _check(load().falcon_cc(g.handle, _style(style), _ptr(label_out), ctypes.byref(st)))
+    return st
+
+
+def falcon_set_profiling(g: Graph, enable: bool):
+    _check(load().falcon_set_profiling(g.handle, int(bool(enable))))
+
+
+def falcon_last_error() -> str:
+    return (load().falcon_last_error() or b"").decode()
+
+
+def falcon_version() -> str:
+    return load().falcon_version().decode()
+
+
+def run(g: Graph, algo: str, style, out, source: int = 0) -> FalconStats:
+    """Dispatch helper: algo in {'sssp','bfs','cc'}."""
+    if algo == "sssp":
+        return falcon_sssp(g, source, style, out)
+    if algo == "bfs":
+        return falcon_bfs(g, source, style, out)
+    if algo == "cc":
+        return falcon_cc(g, style, out)
+    raise KeyError(algo)

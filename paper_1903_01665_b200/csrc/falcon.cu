@@ -1,0 +1,413 @@
+// falcon.cu -- C ABI (include/falcon.h), device graph store and the
+// single-GPU fixpoint driver.
+//
+// Driver: one fused init kernel, then a CUDA graph whose WHILE
+// conditional node runs one round per trip -- relax kernel(s) followed by a
+// one-thread advance kernel that decides on the device whether to continue
+// (cudaGraphSetConditional).  No host round trip per round, unlike the
+// per-iteration `changed` copy of the paper's generated code (PAPER.md:1595,
+// 1682-1684).  The graphs are built once per (graph, algorithm,
+// style) and cached.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/falcon.h"
+#include "kernels.cuh"
+
+using namespace fk;
+
+namespace {
+
+constexpr int BLOCK = 256;
+constexpr int IPT_V = 4;   // vertices per thread per tile (VERTEX style)
+constexpr int IPT_W = 1;   // frontier items per thread per tile (WORKLIST style)
+constexpr int UNROLL = 4;  // arcs per thread per expansion step
+constexpr int HOST_CHECK_EVERY = 4;
+
+thread_local std::string g_last_error;
+
+falcon_status_t fail(falcon_status_t st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+#define CU(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t _e = (call);                                                                      \
+        if (_e != cudaSuccess) {                                                                      \
+            if (_e == cudaErrorMemoryAllocation)                                                      \
+                return fail(FALCON_ERR_NO_MEMORY, "%s: %s", #call, cudaGetErrorString(_e));           \
+            return fail(FALCON_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+        }                                                                                             \
+    } while (0)
+
+template <typename T>
+cudaError_t dmalloc(T **p, size_t count) {
+    // cudaMalloc returns 256-byte aligned memory: the 16-byte vector loads
+    // of the EDGE kernel and the uint4 tile loads rely on it.
+    return cudaMalloc(reinterpret_cast<void **>(p), (count ? count : 1) * sizeof(T));
+}
+
+}  // namespace
+
+struct falcon_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaStream_t cap_stream = nullptr;
+    int64_t n = 0, m = 0;
+    uint32_t *row_off = nullptr, *col = nullptr, *src = nullptr;
+    int32_t *w = nullptr;
+    int32_t *val = nullptr;
+    uint32_t *stamp = nullptr, *fr0 = nullptr, *fr1 = nullptr;
+    Ctrl *ctrl = nullptr;
+    Ctrl *h_ctrl = nullptr;
+    unsigned long long *cnt = nullptr;
+    int *d_flags = nullptr;
+    int num_sms = 0;
+    int grid_expand_v = 0, grid_expand_w = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    cudaGraph_t graphs[3][3] = {};
+    cudaGraphExec_t execs[3][3] = {};
+    bool profiling = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> pev;
+
+    Args args() const {
+        Args a;
+        a.n = (uint32_t)n; a.m = (uint32_t)m;
+        a.row_off = row_off; a.col = col; a.w = w; a.src = src;
+        a.val = val; a.stamp = stamp; a.fr0 = fr0; a.fr1 = fr1;
+        a.ctrl = ctrl; a.cnt = cnt;
+        return a;
+    }
+};
+
+namespace {
+
+template <int ALGO, int STYLE>
+struct Round {
+    // Launch one round's kernels on `s`.  Returns the number of launches.
+    static int launch(falcon_graph *g, cudaStream_t s, cudaGraphConditionalHandle h, int in_graph,
+                      std::vector<cudaEvent_t> *ev) {
+        Args a = g->args();
+        int launches = 0;
+        if (ev) cudaEventRecord((*ev)[0], s);
+        if (STYLE == VERTEX) {
+            k_expand<ALGO, VERTEX, BLOCK, IPT_V, UNROLL><<<g->grid_expand_v, BLOCK, 0, s>>>(a);
+        } else if (STYLE == WORKLIST) {
+            k_expand<ALGO, WORKLIST, BLOCK, IPT_W, UNROLL><<<g->grid_expand_w, BLOCK, 0, s>>>(a);
+        } else {
+            k_edge<ALGO, BLOCK><<<g->grid_edge, BLOCK, 0, s>>>(a);
+        }
+        launches++;
+        if (ev) cudaEventRecord((*ev)[1], s);
+        if (ALGO == CC) {
+            k_compress<<<g->grid_small, BLOCK, 0, s>>>(a);
+            launches++;
+        }
+        launches++;
+        k_advance<STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches);
+        return launches;
+    }
+};
+
+int launch_round(falcon_graph *g, int algo, int style, cudaStream_t s, cudaGraphConditionalHandle h, int in_graph,
+                 std::vector<cudaEvent_t> *ev) {
+#define R(A, S) \
+    if (algo == A && style == S) return Round<A, S>::launch(g, s, h, in_graph, ev);
+    R(SSSP, VERTEX) R(SSSP, EDGE) R(SSSP, WORKLIST)
+    R(BFS, VERTEX) R(BFS, EDGE) R(BFS, WORKLIST)
+    R(CC, VERTEX) R(CC, EDGE) R(CC, WORKLIST)
+#undef R
+    return 0;
+}
+
+falcon_status_t build_graph(falcon_graph *g, int algo, int style) {
+    if (g->execs[algo][style]) return FALCON_OK;
+    cudaGraph_t G;
+    CU(cudaGraphCreate(&G, 0));
+    cudaGraphConditionalHandle h;
+    CU(cudaGraphConditionalHandleCreate(&h, G, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CU(cudaGraphAddNode(&node, G, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CU(cudaStreamBeginCaptureToGraph(g->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    launch_round(g, algo, style, g->cap_stream, h, 1, nullptr);
+    cudaGraph_t captured;
+    cudaError_t e = cudaStreamEndCapture(g->cap_stream, &captured);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(G);
+        return fail(FALCON_ERR_CUDA, "stream capture of the round body failed: %s", cudaGetErrorString(e));
+    }
+    cudaGraphExec_t X;
+    e = cudaGraphInstantiate(&X, G, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(G);
+        return fail(FALCON_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+    }
+    g->graphs[algo][style] = G;
+    g->execs[algo][style] = X;
+    return FALCON_OK;
+}
+
+falcon_status_t ensure_src(falcon_graph *g) {
+    if (g->src || g->m == 0) {
+        if (!g->src) CU(dmalloc(&g->src, 4));
+        return FALCON_OK;
+    }
+    CU(dmalloc(&g->src, (size_t)g->m));
+    k_build_src<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->n, (uint32_t)g->m, g->row_off, g->src);
+    CU(cudaGetLastError());
+    return FALCON_OK;
+}
+
+falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out, falcon_stats_t *stats) {
+    if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
+    if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
+    if (style < 0 || style > 2) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
+    if (algo != CC && (int64_t)source >= g->n) return fail(FALCON_ERR_INVALID_ARG, "source %u >= n", source);
+    CU(cudaSetDevice(g->device));
+    if (style == EDGE) {
+        falcon_status_t st = ensure_src(g);
+        if (st != FALCON_OK) return st;
+    }
+    cudaStream_t s = g->stream;
+    Args a = g->args();
+    const uint32_t cap = (uint32_t)(g->n + 2 > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : g->n + 2);
+    CU(cudaEventRecord(g->ev0, s));
+    if (algo == SSSP) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots);
+    else if (algo == BFS) k_init<BFS><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots);
+    else k_init<CC><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots);
+    CU(cudaGetLastError());
+
+    double relax_ms = -1.0;
+    int64_t relax_launches = 0;
+    if (!g->profiling) {
+        falcon_status_t st = build_graph(g, algo, style);
+        if (st != FALCON_OK) return st;
+        CU(cudaGraphLaunch(g->execs[algo][style], s));
+    } else {
+        // Host-driven loop with CUDA events around every relax launch.
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pairs;
+        size_t next_ev = 0;
+        for (;;) {
+            for (int k = 0; k < HOST_CHECK_EVERY; k++) {
+                while (g->pev.size() < next_ev + 2) {
+                    cudaEvent_t e;
+                    CU(cudaEventCreate(&e));
+                    g->pev.push_back(e);
+                }
+                std::vector<cudaEvent_t> ev = {g->pev[next_ev], g->pev[next_ev + 1]};
+                pairs.push_back({ev[0], ev[1]});
+                next_ev += 2;
+                launch_round(g, algo, style, s, 0, 0, &ev);
+            }
+            CU(cudaGetLastError());
+            CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            if (g->h_ctrl->done) break;
+        }
+        const uint32_t rounds = g->h_ctrl->iter;
+        relax_ms = 0.0;
+        for (size_t i = 0; i < pairs.size() && i < rounds; i++) {
+            float t = 0.f;
+            CU(cudaEventElapsedTime(&t, pairs[i].first, pairs[i].second));
+            relax_ms += t;
+            relax_launches++;
+        }
+    }
+    k_finish<<<1, BLOCK, 0, s>>>(a, (uint32_t)g->cnt_slots);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(g->ev1, s));
+    CU(cudaMemcpyAsync(out, g->val, (size_t)g->n * sizeof(int32_t), cudaMemcpyDefault, s));
+    CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const Ctrl &c = *g->h_ctrl;
+    if (stats) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        stats->iterations = c.iter;
+        stats->vertices_processed = (int64_t)c.vertices;
+        stats->edges_relaxed = (int64_t)c.edges;
+        stats->updates = (int64_t)c.updates;
+        stats->kernel_launches = (int64_t)c.launches;
+        stats->ms = ms;
+        stats->relax_ms = relax_ms;
+        stats->relax_launches = relax_launches;
+    }
+    if (c.status == ST_OVERFLOW) return fail(FALCON_ERR_OVERFLOW, "a finite distance would reach FALCON_INF");
+    if (c.status == ST_NOT_CONVERGED) return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", cap);
+    g_last_error.clear();
+    return FALCON_OK;
+}
+
+void destroy(falcon_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    for (auto &row : g->execs)
+        for (auto &x : row)
+            if (x) cudaGraphExecDestroy(x);
+    for (auto &row : g->graphs)
+        for (auto &x : row)
+            if (x) cudaGraphDestroy(x);
+    for (auto e : g->pev) cudaEventDestroy(e);
+    if (g->ev0) cudaEventDestroy(g->ev0);
+    if (g->ev1) cudaEventDestroy(g->ev1);
+    cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->src);
+    cudaFree(g->val); cudaFree(g->stamp); cudaFree(g->fr0); cudaFree(g->fr1);
+    cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
+    if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
+    if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+    if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+}
+
+falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col, const int32_t *w,
+                     const falcon_load_opts_t *opts, falcon_graph *g) {
+    int dev = opts ? opts->device : -1;
+    if (dev < 0) CU(cudaGetDevice(&dev));
+    g->device = dev;
+    CU(cudaSetDevice(dev));
+    CU(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    if (opts && opts->cuda_stream) {
+        g->stream = (cudaStream_t)opts->cuda_stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        g->own_stream = true;
+    }
+    CU(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&g->ev0));
+    CU(cudaEventCreate(&g->ev1));
+    g->n = n; g->m = m;
+    cudaStream_t s = g->stream;
+
+    CU(dmalloc(&g->row_off, (size_t)n + 1));
+    CU(dmalloc(&g->col, (size_t)m));
+    CU(dmalloc(&g->w, (size_t)m));
+    CU(dmalloc(&g->val, (size_t)n));
+    CU(dmalloc(&g->stamp, (size_t)n));
+    CU(dmalloc(&g->fr0, (size_t)n));
+    CU(dmalloc(&g->fr1, (size_t)n));
+    CU(dmalloc(&g->ctrl, 1));
+    CU(dmalloc(&g->d_flags, 1));
+    CU(cudaMallocHost(&g->h_ctrl, sizeof(Ctrl)));
+
+    CU(cudaMemcpyAsync(g->row_off, row_off, ((size_t)n + 1) * 4, cudaMemcpyDefault, s));
+    if (m) CU(cudaMemcpyAsync(g->col, col, (size_t)m * 4, cudaMemcpyDefault, s));
+    if (m && w) CU(cudaMemcpyAsync(g->w, w, (size_t)m * 4, cudaMemcpyDefault, s));
+    if (m && !w) k_fill_i32<<<g->num_sms * 8, BLOCK, 0, s>>>(g->w, (uint64_t)m, 1);
+
+    // grid sizes: a multiple of the SM count x resident CTAs, capped by the work
+    int occ_v = 0, occ_w = 0, occ_e = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_v, k_expand<SSSP, VERTEX, BLOCK, IPT_V, UNROLL>, BLOCK, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_expand<SSSP, WORKLIST, BLOCK, IPT_W, UNROLL>, BLOCK, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK>, BLOCK, 0));
+    auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };
+    g->grid_expand_v = clampg((n + BLOCK * IPT_V - 1) / (BLOCK * IPT_V), (int64_t)g->num_sms * (occ_v ? occ_v : 1));
+    g->grid_expand_w = clampg((n + BLOCK * IPT_W - 1) / (BLOCK * IPT_W), (int64_t)g->num_sms * (occ_w ? occ_w : 1));
+    g->grid_edge = clampg((m / 4 + 1 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * (occ_e ? occ_e : 1));
+    g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
+    int slots = g->grid_expand_v;
+    if (g->grid_expand_w > slots) slots = g->grid_expand_w;
+    if (g->grid_edge > slots) slots = g->grid_edge;
+    g->cnt_slots = slots;
+    CU(dmalloc(&g->cnt, 3 * (size_t)slots));
+
+    CU(cudaMemsetAsync(g->d_flags, 0, sizeof(int), s));
+    k_validate<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, (uint32_t)m, g->row_off, g->col, w ? g->w : nullptr,
+                                                 g->d_flags);
+    CU(cudaGetLastError());
+    int flags = 0;
+    CU(cudaMemcpyAsync(&flags, g->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (flags & 1) return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must start at 0, be nondecreasing and end at m");
+    if (flags & 2) return fail(FALCON_ERR_OUT_OF_RANGE, "col[e] >= n");
+    if (flags & 4) return fail(FALCON_ERR_OUT_OF_RANGE, "negative weight");
+    if (opts && (opts->flags & FALCON_LOAD_BUILD_COO)) {
+        falcon_status_t st = ensure_src(g);
+        if (st != FALCON_OK) return st;
+        CU(cudaStreamSynchronize(s));
+    }
+    return FALCON_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col, const int32_t *w,
+                               const falcon_load_opts_t *opts, falcon_graph_t **out) {
+    if (!out) return fail(FALCON_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || n >= (1ll << 31)) return fail(FALCON_ERR_INVALID_ARG, "n must be in [1, 2^31)");
+    if (m < 0 || m >= (1ll << 32)) return fail(FALCON_ERR_INVALID_ARG, "m must be in [0, 2^32)");
+    if (!row_off || (m > 0 && !col)) return fail(FALCON_ERR_INVALID_ARG, "row_off/col is NULL");
+    if (opts && (opts->flags & ~(uint32_t)FALCON_LOAD_BUILD_COO))
+        return fail(FALCON_ERR_UNSUPPORTED, "unknown load flags 0x%x", opts->flags);
+    falcon_graph *g = new (std::nothrow) falcon_graph();
+    if (!g) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    falcon_status_t st = load(n, m, row_off, col, w, opts, g);
+    if (st != FALCON_OK) {
+        std::string msg = g_last_error;
+        destroy(g);
+        g_last_error = msg;
+        return st;
+    }
+    g_last_error.clear();
+    *out = g;
+    return FALCON_OK;
+}
+
+falcon_status_t graph_free(falcon_graph_t *g) {
+    destroy(g);
+    return FALCON_OK;
+}
+
+falcon_status_t graph_info(const falcon_graph_t *g, int64_t *n, int64_t *m) {
+    if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
+    if (n) *n = g->n;
+    if (m) *m = g->m;
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_sssp(falcon_graph_t *g, uint32_t source, falcon_style_t style, int32_t *dist_out,
+                            falcon_stats_t *stats) {
+    return run(g, SSSP, source, (int)style, dist_out, stats);
+}
+
+falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon_style_t style, int32_t *level_out,
+                           falcon_stats_t *stats) {
+    return run(g, BFS, source, (int)style, level_out, stats);
+}
+
+falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats) {
+    return run(g, CC, 0, (int)style, label_out, stats);
+}
+
+falcon_status_t falcon_set_profiling(falcon_graph_t *g, int enable) {
+    if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
+    g->profiling = enable != 0;
+    return FALCON_OK;
+}
+
+const char *falcon_last_error(void) { return g_last_error.c_str(); }
+
+const char *falcon_version(void) { return "falcon-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

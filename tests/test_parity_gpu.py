@@ -1,0 +1,252 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bit-exact equality on every output (all three outputs are unique integer
+fixpoints), for SSSP / BFS / CC x VERTEX / EDGE / WORKLIST, on
+the SPEC.md goldens, edge cases, reduced-scale graphs that span many tiles
+with ragged tails, and the full BASELINE.json configs (rand-25M, rmat-10M,
+grid-24M) in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+import torch
+
+import graphgen as gg
+import oracle
+from common import INF, cert_bfs, cert_sssp, golden_files, load_golden
+
+pytestmark = pytest.mark.gpu
+ALGOS = ["sssp", "bfs", "cc"]
+STYLES = ["vertex", "edge", "worklist"]
+
+
+def _load(fb, n, row_off, col, w, device_inputs=False):
+    if device_inputs:
+        t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        return fb.graph_load_csr(n, len(col), t(row_off), t(col), t(w), device=0)
+    return fb.graph_load_csr(n, len(col), row_off, col, w, device=0)
+
+
+def _run(fb, g, algo, style, source, device_out=False):
+    if device_out:
+        out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        st = fb.run(g, algo, style, out, source)
+        return out.cpu().numpy(), st
+    out = np.empty(g.n, np.int32)
+    st = fb.run(g, algo, style, out, source)
+    return out, st
+
+
+def _oracle(algo, row_off, col, w, s):
+    if algo == "sssp":
+        return oracle.sssp(row_off, col, w, s)
+    if algo == "bfs":
+        return oracle.bfs(row_off, col, s)
+    return oracle.cc(row_off, col)
+
+
+# ------------------------------------------------------------------ goldens
+@pytest.mark.parametrize("fname", golden_files())
+@pytest.mark.parametrize("style", STYLES)
+def test_golden(gpu_lib, fname, style):
+    gd = load_golden(fname)
+    row_off, col, w = gg.csr_from_edges(gd.n, gd.src, gd.dst, gd.w)
+    g = _load(gpu_lib, gd.n, row_off, col, w)
+    for algo in ALGOS:
+        if algo in gd.expect:
+            out, _ = _run(gpu_lib, g, algo, style, gd.source)
+            assert np.array_equal(out, gd.expect[algo]), (fname, algo, style, out)
+
+
+# ------------------------------------------------------------------ reduced scale, many tiles
+def _ragged():
+    # m % 4 == 3 (EDGE tail), n not a multiple of any tile size
+    s, d, w = gg.er_edges(100_003, 400_011, 77)
+    return gg.from_edges("ragged", 100_003, s, d, w, seed=77)
+
+
+GRAPHS = {
+    "tiny": lambda: gg.config("tiny"),
+    "rand-s": lambda: gg.config("rand-s"),
+    "rmat-s": lambda: gg.config("rmat-s"),
+    "grid-s": lambda: gg.config("grid-s"),
+    "ragged": _ragged,
+}
+_cache = {}
+
+
+def _graph(name):
+    if name not in _cache:
+        _cache[name] = GRAPHS[name]()
+    return _cache[name]
+
+
+@pytest.mark.parametrize("name", list(GRAPHS))
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("style", STYLES)
+def test_parity_small(gpu_lib, name, algo, style):
+    G = _graph(name)
+    exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    out, st = _run(gpu_lib, g, algo, style, G.source)
+    assert np.array_equal(out, exp), f"{name}/{algo}/{style}: {np.flatnonzero(out != exp)[:10]}"
+    assert st.iterations >= 1 and st.kernel_launches >= 2
+
+
+def test_device_inputs_and_outputs(gpu_lib):
+    G = _graph("rmat-s")
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w, device_inputs=True)
+    for algo in ALGOS:
+        exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+        for style in STYLES:
+            out, _ = _run(gpu_lib, g, algo, style, G.source, device_out=True)
+            assert np.array_equal(out, exp)
+
+
+def test_repeat_and_profiling_mode_identical(gpu_lib):
+    G = _graph("rand-s")
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    for algo in ALGOS:
+        exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+        for style in STYLES:
+            a, s1 = _run(gpu_lib, g, algo, style, G.source)
+            b, _ = _run(gpu_lib, g, algo, style, G.source)
+            gpu_lib.falcon_set_profiling(g, True)
+            c, sp = _run(gpu_lib, g, algo, style, G.source)
+            gpu_lib.falcon_set_profiling(g, False)
+            assert np.array_equal(a, exp) and np.array_equal(b, exp) and np.array_equal(c, exp)
+            assert sp.relax_ms > 0 and sp.relax_launches == sp.iterations
+            assert s1.relax_ms == -1.0
+
+
+def test_many_sources(gpu_lib):
+    G = _graph("rmat-s")
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    rng = np.random.default_rng(5)
+    for s in rng.integers(0, G.n, 6):
+        s = int(s)
+        for algo in ("sssp", "bfs"):
+            exp = _oracle(algo, G.row_off, G.col, G.w, s)
+            for style in STYLES:
+                out, _ = _run(gpu_lib, g, algo, style, s)
+                assert np.array_equal(out, exp)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_single_vertex_no_arcs(gpu_lib):
+    row_off = np.zeros(2, np.uint32); col = np.zeros(0, np.uint32)
+    g = gpu_lib.graph_load_csr(1, 0, row_off, col, None, device=0)
+    for style in STYLES:
+        for algo in ALGOS:
+            out, _ = _run(gpu_lib, g, algo, style, 0)
+            assert out.tolist() == [0]
+
+
+def test_no_arcs(gpu_lib):
+    n = 5000
+    row_off = np.zeros(n + 1, np.uint32); col = np.zeros(0, np.uint32)
+    g = gpu_lib.graph_load_csr(n, 0, row_off, col, np.zeros(0, np.int32), device=0)
+    for style in STYLES:
+        d, _ = _run(gpu_lib, g, "sssp", style, 17)
+        exp = np.full(n, INF, np.int32); exp[17] = 0
+        assert np.array_equal(d, exp)
+        l, _ = _run(gpu_lib, g, "cc", style, 0)
+        assert np.array_equal(l, np.arange(n, dtype=np.int32))
+
+
+def test_isolated_source(gpu_lib):
+    G = _graph("rand-s")
+    deg = G.out_degree()
+    iso = int(np.flatnonzero(deg == 0)[0])
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    for style in STYLES:
+        d, _ = _run(gpu_lib, g, "sssp", style, iso)
+        assert d[iso] == 0 and (np.delete(d, iso) == INF).all()
+
+
+def test_unit_weights_null_w(gpu_lib):
+    G = _graph("grid-s")
+    g = gpu_lib.graph_load_csr(G.n, G.m, G.row_off, G.col, None, device=0)
+    exp = oracle.bfs(G.row_off, G.col, G.source)
+    for style in STYLES:
+        d, _ = _run(gpu_lib, g, "sssp", style, G.source)
+        assert np.array_equal(d, exp)
+
+
+def test_zero_weights_self_loops_duplicates(gpu_lib):
+    rng = np.random.default_rng(11)
+    n, m = 20_000, 90_001
+    s = rng.integers(0, n, m).astype(np.uint32); d = rng.integers(0, n, m).astype(np.uint32)
+    s[:500] = d[:500]  # self loops
+    s = np.concatenate([s, s[:7000]]); d = np.concatenate([d, d[:7000]])
+    w = rng.integers(0, 3, len(s)).astype(np.int32)
+    row_off, col, wc = gg.csr_from_edges(n, s, d, w)
+    g = gpu_lib.graph_load_csr(n, len(col), row_off, col, wc, device=0)
+    for algo in ALGOS:
+        exp = _oracle(algo, row_off, col, wc, 3)
+        for style in STYLES:
+            out, _ = _run(gpu_lib, g, algo, style, 3)
+            assert np.array_equal(out, exp)
+
+
+def test_star_hub(gpu_lib):
+    """One hub with 200k out-arcs (degree far above a tile) plus in-arcs."""
+    n = 200_001
+    s = np.concatenate([np.zeros(n - 1, np.uint32), np.arange(1, n, dtype=np.uint32)])
+    d = np.concatenate([np.arange(1, n, dtype=np.uint32), np.zeros(n - 1, np.uint32)])
+    w = (np.arange(len(s)) % 97 + 1).astype(np.int32)
+    row_off, col, wc = gg.csr_from_edges(n, s, d, w)
+    g = gpu_lib.graph_load_csr(n, len(col), row_off, col, wc, device=0)
+    for algo in ALGOS:
+        exp = _oracle(algo, row_off, col, wc, 5)
+        for style in STYLES:
+            out, _ = _run(gpu_lib, g, algo, style, 5)
+            assert np.array_equal(out, exp)
+
+
+def test_overflow_status(gpu_lib):
+    row_off, col, w = gg.csr_from_edges(4, np.array([0, 1, 2], np.uint32), np.array([1, 2, 3], np.uint32),
+                                        np.array([1 << 30] * 3, np.int32))
+    g = gpu_lib.graph_load_csr(4, 3, row_off, col, w, device=0)
+    for style in STYLES:
+        with pytest.raises(gpu_lib.FalconError) as ei:
+            _run(gpu_lib, g, "sssp", style, 0)
+        assert ei.value.name == "OVERFLOW"
+
+
+def test_load_validation(gpu_lib):
+    fb = gpu_lib
+    ro = np.array([0, 2, 3, 3], np.uint32)
+    with pytest.raises(fb.FalconError) as e:
+        fb.graph_load_csr(3, 3, ro, np.array([1, 5, 2], np.uint32), None, device=0)
+    assert e.value.name == "OUT_OF_RANGE"
+    with pytest.raises(fb.FalconError) as e:
+        fb.graph_load_csr(3, 3, ro, np.array([1, 2, 2], np.uint32), np.array([1, -1, 1], np.int32), device=0)
+    assert e.value.name == "OUT_OF_RANGE"
+    with pytest.raises(fb.FalconError) as e:
+        fb.graph_load_csr(3, 3, np.array([0, 3, 2, 3], np.uint32), np.array([1, 2, 2], np.uint32), None, device=0)
+    assert e.value.name == "OUT_OF_RANGE"
+    g = fb.graph_load_csr(3, 3, ro, np.array([1, 2, 2], np.uint32), None, device=0)
+    with pytest.raises(fb.FalconError) as e:
+        fb.falcon_sssp(g, 3, "vertex", np.empty(3, np.int32))
+    assert e.value.name == "INVALID_ARG"
+    with pytest.raises(fb.FalconError) as e:
+        fb.falcon_bfs(g, 0, 7, np.empty(3, np.int32))
+    assert e.value.name == "INVALID_ARG"
+
+
+# ------------------------------------------------------------------ full BASELINE.json configs
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["rand-25M", "rmat-10M", "grid-24M"])
+def test_parity_full_config(gpu_lib, name):
+    G = gg.config(name)
+    g = gpu_lib.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0)
+    out = np.empty(G.n, np.int32)
+    for algo in ALGOS:
+        exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+        for style in STYLES:
+            gpu_lib.run(g, algo, style, out, G.source)
+            assert np.array_equal(out, exp), f"{name}/{algo}/{style}"
+        if algo == "sssp":
+            cert_sssp(G.row_off, G.col, G.w, G.source, exp)
+        elif algo == "bfs":
+            cert_bfs(G.row_off, G.col, G.source, exp)
