@@ -13,7 +13,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/falcon.h"
@@ -24,9 +26,10 @@ using namespace fk;
 namespace {
 
 constexpr int BLOCK = 256;
-constexpr int IPT_V = 4;   // vertices per thread per tile (VERTEX style)
-constexpr int IPT_W = 1;   // frontier items per thread per tile (WORKLIST style)
-constexpr int UNROLL = 4;  // arcs per thread per expansion step
+constexpr int IPT_ALL = 4;  // items per thread per tile when every vertex is an item (CC VERTEX)
+constexpr int IPT_FR = 1;   // frontier items per thread per tile
+constexpr int UNROLL = 4;   // arcs per thread per expansion step
+constexpr int MINB = 4;     // min resident CTAs per SM for the warp-centric expansion
 constexpr int HOST_CHECK_EVERY = 4;
 
 thread_local std::string g_last_error;
@@ -69,30 +72,55 @@ struct falcon_graph {
     uint32_t *row_off = nullptr, *col = nullptr, *src = nullptr;
     int32_t *w = nullptr;
     int32_t *val = nullptr;
-    uint32_t *stamp = nullptr, *fr0 = nullptr, *fr1 = nullptr;
+    uint32_t *bm = nullptr, *fr0 = nullptr, *fr1 = nullptr;   // bm: 4 bitmaps of nwords
+    uint32_t nwords = 0;
     Ctrl *ctrl = nullptr;
     Ctrl *h_ctrl = nullptr;
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_expand_v = 0, grid_expand_w = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    int grid_expand_all = 0, grid_expand_fr = 0, grid_scan = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
     cudaGraph_t graphs[3][3] = {};
     cudaGraphExec_t execs[3][3] = {};
     bool profiling = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> pev;
+    bool warp_expand = true;             // warp-centric expansion (FALCON_EXPAND=cta for the CTA-tile kernel)
+    bool l2_window = false;              // persisting L2 access-policy window on val[]
+    cudaAccessPolicyWindow apw = {};
 
     Args args() const {
         Args a;
-        a.n = (uint32_t)n; a.m = (uint32_t)m;
+        a.n = (uint32_t)n; a.m = (uint32_t)m; a.nwords = nwords;
         a.row_off = row_off; a.col = col; a.w = w; a.src = src;
-        a.val = val; a.stamp = stamp; a.fr0 = fr0; a.fr1 = fr1;
+        a.val = val; a.fr0 = fr0; a.fr1 = fr1;
+        a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
         return a;
     }
 };
 
 namespace {
+
+// Launch a relax-round kernel with the graph's L2 access-policy window (the
+// gathered value array is marked persisting so the streamed CSR/COO arrays do
+// not evict it).  Inside stream capture the attribute becomes
+// a kernel-node attribute.
+template <typename... KArgs, typename... Act>
+void launch_l2(const falcon_graph *g, void (*k)(KArgs...), int grid, cudaStream_t s, Act &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(BLOCK);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (g->l2_window) {
+        at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[0].val.accessPolicyWindow = g->apw;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...);
+}
 
 template <int ALGO, int STYLE>
 struct Round {
@@ -102,17 +130,24 @@ struct Round {
         Args a = g->args();
         int launches = 0;
         if (ev) cudaEventRecord((*ev)[0], s);
-        if (STYLE == VERTEX) {
-            k_expand<ALGO, VERTEX, BLOCK, IPT_V, UNROLL><<<g->grid_expand_v, BLOCK, 0, s>>>(a);
+        if (STYLE == VERTEX && ALGO == CC) {
+            if (g->warp_expand) launch_l2(g, k_expand_warp<ALGO, VERTEX, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a);
+            else launch_l2(g, k_expand<ALGO, VERTEX, BLOCK, IPT_ALL, UNROLL>, g->grid_expand_all, s, a);
+        } else if (STYLE == VERTEX) {
+            launch_l2(g, k_scan<BLOCK>, g->grid_scan, s, a);
+            launches++;
+            if (g->warp_expand) launch_l2(g, k_expand_warp<ALGO, VERTEX, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a);
+            else launch_l2(g, k_expand<ALGO, VERTEX, BLOCK, IPT_FR, UNROLL>, g->grid_expand_fr, s, a);
         } else if (STYLE == WORKLIST) {
-            k_expand<ALGO, WORKLIST, BLOCK, IPT_W, UNROLL><<<g->grid_expand_w, BLOCK, 0, s>>>(a);
+            if (g->warp_expand) launch_l2(g, k_expand_warp<ALGO, WORKLIST, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a);
+            else launch_l2(g, k_expand<ALGO, WORKLIST, BLOCK, IPT_FR, UNROLL>, g->grid_expand_fr, s, a);
         } else {
-            k_edge<ALGO, BLOCK><<<g->grid_edge, BLOCK, 0, s>>>(a);
+            launch_l2(g, k_edge<ALGO, BLOCK>, g->grid_edge, s, a);
         }
         launches++;
         if (ev) cudaEventRecord((*ev)[1], s);
         if (ALGO == CC) {
-            k_compress<<<g->grid_small, BLOCK, 0, s>>>(a);
+            launch_l2(g, k_compress, g->grid_small, s, a);
             launches++;
         }
         launches++;
@@ -190,9 +225,9 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     Args a = g->args();
     const uint32_t cap = (uint32_t)(g->n + 2 > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : g->n + 2);
     CU(cudaEventRecord(g->ev0, s));
-    if (algo == SSSP) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots);
-    else if (algo == BFS) k_init<BFS><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots);
-    else k_init<CC><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots);
+    if (algo == SSSP) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style);
+    else if (algo == BFS) k_init<BFS><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style);
+    else k_init<CC><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style);
     CU(cudaGetLastError());
 
     double relax_ms = -1.0;
@@ -270,7 +305,7 @@ void destroy(falcon_graph *g) {
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
     cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->src);
-    cudaFree(g->val); cudaFree(g->stamp); cudaFree(g->fr0); cudaFree(g->fr1);
+    cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1);
     cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -301,7 +336,8 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     CU(dmalloc(&g->col, (size_t)m));
     CU(dmalloc(&g->w, (size_t)m));
     CU(dmalloc(&g->val, (size_t)n));
-    CU(dmalloc(&g->stamp, (size_t)n));
+    g->nwords = (uint32_t)((((n + 31) / 32) + 3) & ~3ll);
+    CU(dmalloc(&g->bm, 4 * (size_t)g->nwords));
     CU(dmalloc(&g->fr0, (size_t)n));
     CU(dmalloc(&g->fr1, (size_t)n));
     CU(dmalloc(&g->ctrl, 1));
@@ -314,20 +350,50 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (m && !w) k_fill_i32<<<g->num_sms * 8, BLOCK, 0, s>>>(g->w, (uint64_t)m, 1);
 
     // grid sizes: a multiple of the SM count x resident CTAs, capped by the work
-    int occ_v = 0, occ_w = 0, occ_e = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_v, k_expand<SSSP, VERTEX, BLOCK, IPT_V, UNROLL>, BLOCK, 0));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_expand<SSSP, WORKLIST, BLOCK, IPT_W, UNROLL>, BLOCK, 0));
+    int occ_a = 0, occ_f = 0, occ_e = 0, occ_s = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_expand<CC, VERTEX, BLOCK, IPT_ALL, UNROLL>, BLOCK, 0));
+    const char *ex = getenv("FALCON_EXPAND");
+    g->warp_expand = !(ex && strcmp(ex, "cta") == 0);
+    if (g->warp_expand)
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_expand_warp<SSSP, WORKLIST, BLOCK, UNROLL, MINB>, BLOCK, 0));
+    else
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_expand<SSSP, WORKLIST, BLOCK, IPT_FR, UNROLL>, BLOCK, 0));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK>, BLOCK, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scan<BLOCK>, BLOCK, 0));
     auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };
-    g->grid_expand_v = clampg((n + BLOCK * IPT_V - 1) / (BLOCK * IPT_V), (int64_t)g->num_sms * (occ_v ? occ_v : 1));
-    g->grid_expand_w = clampg((n + BLOCK * IPT_W - 1) / (BLOCK * IPT_W), (int64_t)g->num_sms * (occ_w ? occ_w : 1));
-    g->grid_edge = clampg((m / 4 + 1 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * (occ_e ? occ_e : 1));
+    auto full = [&](int occ) { return (int64_t)g->num_sms * (occ > 0 ? occ : 1); };
+    g->grid_expand_all = clampg((n + BLOCK * IPT_ALL - 1) / (BLOCK * IPT_ALL), full(occ_a));
+    g->grid_expand_fr = clampg((n + BLOCK * IPT_FR - 1) / (BLOCK * IPT_FR), full(occ_f));
+    g->grid_edge = clampg((m / 4 + 1 + BLOCK - 1) / BLOCK, full(occ_e));
+    g->grid_scan = clampg((g->nwords / 4 + BLOCK - 1) / BLOCK, full(occ_s));
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
-    int slots = g->grid_expand_v;
-    if (g->grid_expand_w > slots) slots = g->grid_expand_w;
+    int slots = g->grid_expand_all;
+    if (g->grid_expand_fr > slots) slots = g->grid_expand_fr;
     if (g->grid_edge > slots) slots = g->grid_edge;
     g->cnt_slots = slots;
     CU(dmalloc(&g->cnt, 3 * (size_t)slots));
+
+    // Persisting L2 window over the gathered value array (opt out: FALCON_L2_PERSIST=0).
+    const char *env = getenv("FALCON_L2_PERSIST");
+    if (!(env && env[0] == '0')) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (max_persist > 0 && max_window > 0) {
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            if (cur < (size_t)max_persist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+            const size_t bytes = (size_t)n * sizeof(int32_t);
+            g->apw.base_ptr = g->val;
+            g->apw.num_bytes = bytes < (size_t)max_window ? bytes : (size_t)max_window;
+            const double ratio = (double)max_persist / (double)g->apw.num_bytes;
+            g->apw.hitRatio = (float)(ratio < 1.0 ? ratio : 1.0);
+            g->apw.hitProp = cudaAccessPropertyPersisting;
+            g->apw.missProp = cudaAccessPropertyStreaming;
+            g->l2_window = true;
+        }
+        cudaGetLastError();
+    }
 
     CU(cudaMemsetAsync(g->d_flags, 0, sizeof(int), s));
     k_validate<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, (uint32_t)m, g->row_off, g->col, w ? g->w : nullptr,

@@ -5,14 +5,21 @@
 // an atomicMin on a 32-bit integer array, applied to every ACTIVE arc p->t
 // until a round changes nothing.  The three processing styles differ only in
 // which arcs a round visits:
-//   VERTEX   -- every vertex of the CSR whose value changed in the previous
-//               round (topology-driven; the activity
-//               filter leaves the fixpoint unchanged, R8),
+//   VERTEX   -- every vertex is visited (topology-driven, PAPER.md:1683
+//               "foreach (t In graph.points)"); those whose value changed in
+//               the previous round (R8) / whose level is lev (BFS,
+//               PAPER.md:1322) expand their CSR row,
 //   EDGE     -- every arc of the COO array with an active source
 //               (PAPER.md:1694-1725),
 //   WORKLIST -- the vertices of a frontier queue.
 // BFS uses the level-synchronous update of PAPER.md:1306-1313; CC hooks
 // minimum labels and pointer-jumps (reading R6).
+//
+// Activity sets are bitmaps (n bits, a few MB, L2-resident): bm[r % 3] holds
+// the vertices improved in round r; round r reads bm[(r-1) % 3], writes
+// bm[r % 3] and clears bm[(r+1) % 3] for the next round.  BFS also keeps a
+// visited bitmap.  The value array is gathered with an L2 evict-last policy,
+// the streamed CSR/COO arrays with evict-first.
 //
 // Nothing here shares code with oracle/ (DESIGN.md §4).
 #pragma once
@@ -21,8 +28,7 @@
 
 namespace fk {
 
-constexpr int32_t INF = 0x7fffffff;           // MAX_INT
-constexpr uint32_t NO_STAMP = 0xffffffffu;
+constexpr int32_t INF = 0x7fffffff;   // MAX_INT
 constexpr unsigned FULL = 0xffffffffu;
 
 enum Algo : int { SSSP = 0, BFS = 1, CC = 2 };
@@ -34,13 +40,13 @@ enum DevStatus : int { ST_OK = 0, ST_OVERFLOW = 5, ST_NOT_CONVERGED = 6 };
 // copy of PAPER.md:1682-1684 / SPEC.md:370).
 struct Ctrl {
     uint32_t iter;        // current round, 1-based
-    uint32_t in_len;      // WORKLIST: items in the input frontier
+    uint32_t in_len;      // items in the input frontier (VERTEX: built by k_scan)
     uint32_t out_len;     // WORKLIST: items appended to the output frontier
     uint32_t changed;     // VERTEX/EDGE: some value decreased this round
     uint32_t cap;         // round cap (n + 2)
     uint32_t sel;         // WORKLIST: which buffer is the input frontier
     uint32_t done;        // fixpoint reached (or error)
-    uint32_t all_active;  // WORKLIST CC round 1: frontier = all vertices (implicit)
+    uint32_t all_active;  // CC round 1: frontier = all vertices (implicit)
     int32_t status;       // DevStatus
     uint32_t source;
     uint32_t pad0, pad1;
@@ -51,28 +57,68 @@ struct Ctrl {
 };
 
 struct Args {
-    uint32_t n, m;
+    uint32_t n, m, nwords;     // nwords = ceil(n / 32), rounded up to a multiple of 4
     const uint32_t *row_off;   // [n+1]
     const uint32_t *col;       // [m]
     const int32_t *w;          // [m]
     const uint32_t *src;       // [m] COO sources (CSR order), EDGE style only
     int32_t *val;              // dist / level / label [n]
-    uint32_t *stamp;           // [n] round stamps
+    uint32_t *bm0, *bm1, *bm2; // round bitmaps [nwords] each
+    uint32_t *vis;             // BFS visited bitmap [nwords]
     uint32_t *fr0, *fr1;       // frontier queues [n] each
     Ctrl *ctrl;
     unsigned long long *cnt;   // [gridDim.x * 3] per-CTA counters: vertices, edges, updates
 };
 
-// ------------------------------------------------------------------ loads
+__device__ __forceinline__ uint32_t *bm_of(const Args &a, uint32_t r) {
+    const uint32_t k = r % 3u;
+    return k == 0 ? a.bm0 : (k == 1 ? a.bm1 : a.bm2);
+}
+
+// ------------------------------------------------------------------ loads with L2 policies
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// read-only, streamed once per round: no L1 allocation, evict-first in L2
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_stream4(const uint32_t *p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int4 ld_stream4(const int32_t *p, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+// mutable value array (written by atomics in the same kernel): coherent
+// load, evict-last so the gathered array stays L2-resident
+__device__ __forceinline__ int32_t ld_val(const int32_t *p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ uint32_t ld_ro(const uint32_t *p) { return __ldg(p); }
-__device__ __forceinline__ int32_t ld_ro(const int32_t *p) { return __ldg(p); }
-__device__ __forceinline__ uint4 ld_ro4(const uint32_t *p) { return __ldg(reinterpret_cast<const uint4 *>(p)); }
-__device__ __forceinline__ int4 ld_ro4(const int32_t *p) { return __ldg(reinterpret_cast<const int4 *>(p)); }
-// Streamed once per round: evict-first so the gathered value array keeps L2.
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t *p) { return __ldcs(p); }
-__device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p); }
-__device__ __forceinline__ uint4 ld_stream4(const uint32_t *p) { return __ldcs(reinterpret_cast<const uint4 *>(p)); }
-__device__ __forceinline__ int4 ld_stream4(const int32_t *p) { return __ldcs(reinterpret_cast<const int4 *>(p)); }
+
+__device__ __forceinline__ bool bit_test(const uint32_t *bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
 
 // ------------------------------------------------------------------ block primitives
 template <int B>
@@ -97,18 +143,9 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t &total,
     }
     __syncthreads();
     total = s_warp[B / 32 - 1];
-    return (wid ? s_warp[wid - 1] : 0) + v - x;
-}
-
-// Warp-aggregated frontier append: one atomicAdd per warp (ballot + popc).
-__device__ __forceinline__ void warp_append(bool want, uint32_t item, uint32_t *out, uint32_t *counter) {
-    const unsigned mask = __ballot_sync(FULL, want);
-    if (mask == 0) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
-    base = __shfl_sync(FULL, base, leader);
-    if (want) out[base + __popc(mask & ((1u << lane) - 1u))] = item;
+    const uint32_t r = (wid ? s_warp[wid - 1] : 0) + v - x;
+    __syncthreads();   // s_warp may be reused right away
+    return r;
 }
 
 template <int B>
@@ -139,26 +176,71 @@ __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long
     }
 }
 
-// ------------------------------------------------------------------ init (fused)
-// SSSP/BFS: dist = MAX_INT, dist[source] = 0 (PAPER.md:1679-1680, 1318-1319);
-// CC: label[v] = v.  Also seeds the frontier and resets the control block.
-template <int ALGO>
-__global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len) {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += stride) {
-        if (ALGO == CC) {
-            a.val[v] = (int32_t)v;
-            a.stamp[v] = NO_STAMP;
-        } else {
-            a.val[v] = v == source ? 0 : INF;
-            a.stamp[v] = v == source ? 0u : NO_STAMP;
+// Clear the bitmap of round r+1 (grid-stride, 16-byte stores).
+__device__ __forceinline__ void clear_next_bitmap(const Args &a, uint32_t r) {
+    uint4 *p = reinterpret_cast<uint4 *>(bm_of(a, r + 1));
+    const uint32_t n4 = a.nwords >> 2;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x)
+        p[i] = make_uint4(0, 0, 0, 0);
+}
+
+// ------------------------------------------------------------------ block-level frontier queue
+// Appends are staged in shared memory (warp-aggregated shared atomics) and
+// written out with ONE global atomicAdd per flush: a single global counter hit
+// by every warp serialises in one L2 slice.
+template <int B, int QCAP>
+struct BlockQueue {
+    uint32_t *q;      // [QCAP] shared
+    uint32_t *cnt;    // shared
+    uint32_t *base;   // shared
+    __device__ __forceinline__ void push(bool want, uint32_t item) {   // warp-collective
+        const unsigned mask = __ballot_sync(FULL, want);
+        if (mask == 0) return;
+        const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+        uint32_t b = 0;
+        if (lane == leader) b = atomicAdd(cnt, (uint32_t)__popc(mask));
+        b = __shfl_sync(FULL, b, leader);
+        if (want) q[b + __popc(mask & ((1u << lane) - 1u))] = item;
+    }
+    // block-collective; flushes when more than `thresh` items are staged
+    __device__ __forceinline__ void flush(uint32_t *out, uint32_t *gcounter, uint32_t thresh) {
+        __syncthreads();
+        const uint32_t c = *cnt;
+        if (c > thresh) {
+            if (threadIdx.x == 0) *base = atomicAdd(gcounter, c);
+            __syncthreads();
+            const uint32_t b = *base;
+            for (uint32_t i = threadIdx.x; i < c; i += B) out[b + i] = q[i];
+            __syncthreads();
+            if (threadIdx.x == 0) *cnt = 0;
+            __syncthreads();
         }
     }
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt_len; i += stride) a.cnt[i] = 0ull;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+};
+
+// ------------------------------------------------------------------ init (fused)
+// SSSP/BFS: dist = MAX_INT, dist[source] = 0 (PAPER.md:1679-1680, 1318-1319);
+// CC: label[v] = v.  Clears the bitmaps (source bit set in bm0 / vis), seeds
+// the frontier and resets the control block, in one launch.
+template <int ALGO>
+__global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, int style) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t v = t0; v < a.n; v += stride) {
+        if (ALGO == CC) a.val[v] = (int32_t)v;
+        else a.val[v] = v == source ? 0 : INF;
+    }
+    const uint32_t sw = ALGO == CC ? 0xffffffffu : source >> 5, sb = 1u << (source & 31);
+    for (uint32_t i = t0; i < a.nwords; i += stride) {
+        a.bm0[i] = i == sw ? sb : 0u;
+        a.bm1[i] = 0u; a.bm2[i] = 0u;
+        if (ALGO == BFS) a.vis[i] = i == sw ? sb : 0u;
+    }
+    for (uint32_t i = t0; i < cnt_len; i += stride) a.cnt[i] = 0ull;
+    if (t0 == 0) {
         Ctrl *c = a.ctrl;
         c->iter = 1;
-        c->in_len = ALGO == CC ? a.n : 1u;
+        c->in_len = ALGO == CC ? a.n : (style == VERTEX ? 0u : 1u);   // VERTEX: k_scan builds it
         c->out_len = 0; c->changed = 0; c->cap = cap; c->sel = 0; c->done = 0;
         c->all_active = ALGO == CC ? 1u : 0u;
         c->status = ST_OK; c->source = source;
@@ -167,37 +249,83 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len) 
     }
 }
 
+// ------------------------------------------------------------------ VERTEX activity scan
+// Topology-driven round, part 1: visit EVERY vertex through
+// its bit in bm[(r-1)%3] and compact the active ones into the frontier, 128
+// vertices per thread per step (16-byte bitmap loads); one global atomicAdd
+// per CTA step.  Also clears bm[(r+1)%3].
+template <int B>
+__global__ void __launch_bounds__(B) k_scan(Args a) {
+    Ctrl *c = a.ctrl;
+    if (c->done) return;
+    const uint32_t iter = c->iter;
+    clear_next_bitmap(a, iter);
+    const uint4 *bm = reinterpret_cast<const uint4 *>(bm_of(a, iter - 1));
+    __shared__ uint32_t s_warp[B / 32];
+    __shared__ uint32_t s_base;
+    const uint32_t n4 = a.nwords >> 2;
+    for (uint32_t b0 = blockIdx.x * B; b0 < n4; b0 += gridDim.x * B) {   // block-uniform
+        const uint32_t i = b0 + threadIdx.x;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (i < n4) x = bm[i];
+        const uint32_t cnt = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        uint32_t total;
+        uint32_t off = block_excl_scan<B>(cnt, total, s_warp);
+        if (total == 0) continue;
+        if (threadIdx.x == 0) s_base = atomicAdd(&c->in_len, total);
+        __syncthreads();
+        off += s_base;
+        const uint32_t words[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            uint32_t wv = words[j];
+            const uint32_t vb = (4 * i + j) * 32;
+            while (wv) {
+                const int bpos = __ffs(wv) - 1;
+                wv &= wv - 1;
+                a.fr0[off++] = vb + bpos;   // bits beyond n are never set
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ expansion (VERTEX / WORKLIST)
-// A CTA takes a tile of B*IPT items (vertices or frontier entries), each
-// thread IPT consecutive ones; active items contribute their out-degree, a
-// block scan turns degrees into offsets, and the CTA then walks the tile's
-// concatenated arc ranges B*U arcs at a time, each thread finding its item by
-// binary search in shared memory.  Every arc gets one thread regardless of
-// the degree distribution (cooperative expansion for skewed RMAT degrees,
-// PAPER.md:441-446), and consecutive threads read consecutive col/w words.
+// A CTA takes a tile of B*IPT items (frontier entries, or all vertices for
+// CC), each thread IPT consecutive ones; active items contribute their
+// out-degree, a block scan turns degrees into offsets, and the CTA then walks
+// the tile's concatenated arc ranges B*U arcs at a time, each thread finding
+// its item by binary search in shared memory.  Every arc gets one thread
+// regardless of the degree distribution (cooperative expansion for skewed
+// RMAT degrees), and consecutive threads read consecutive
+// col/w words.
+//   VERTEX  : items = the frontier k_scan compacted (CC: all vertices);
+//             an improvement marks v in bm[r%3] / sets `changed`.
+//   WORKLIST: items = the queue of the previous round; an improvement appends
+//             v once per round (bitmap claim).
 template <int ALGO, int STYLE, int B, int IPT, int U>
-__global__ void __launch_bounds__(B) k_expand(Args a) {
+__global__ void __launch_bounds__(B, 4) k_expand(Args a) {
     static_assert(STYLE == VERTEX || STYLE == WORKLIST, "expand is for VERTEX/WORKLIST");
     constexpr int TILE = B * IPT;
+    constexpr int QCAP = STYLE == WORKLIST ? 2 * B * U : 1;
     Ctrl *c = a.ctrl;
     if (c->done) return;
     const uint32_t iter = c->iter;
     const uint32_t lev = iter - 1;   // BFS level being expanded
-    uint32_t nitems;
-    const uint32_t *in = nullptr;
-    uint32_t *out = nullptr;
-    bool implicit = STYLE == VERTEX;
-    if (STYLE == WORKLIST) {
-        nitems = c->in_len;
-        in = c->sel ? a.fr1 : a.fr0;
-        out = c->sel ? a.fr0 : a.fr1;
-        implicit = c->all_active != 0;
-    } else {
-        nitems = a.n;
-    }
+    const uint32_t *in = c->sel ? a.fr1 : a.fr0;
+    uint32_t *out = c->sel ? a.fr0 : a.fr1;
+    const bool implicit = ALGO == CC && (STYLE == VERTEX || c->all_active != 0);
+    const uint32_t nitems = implicit ? a.n : c->in_len;
+    uint32_t *bm_now = bm_of(a, iter);
+    if (STYLE == WORKLIST || ALGO == CC) clear_next_bitmap(a, iter);   // VERTEX SSSP/BFS: k_scan clears
+    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
 
     __shared__ uint32_t s_off[TILE], s_beg[TILE], s_pay[TILE], s_u[TILE];
     __shared__ uint32_t s_warp[B / 32];
+    __shared__ uint32_t s_q[QCAP];
+    __shared__ uint32_t s_cnt, s_base;
+    if (threadIdx.x == 0) s_cnt = 0;
+    BlockQueue<B, QCAP> bq{s_q, &s_cnt, &s_base};
     unsigned long long nv = 0, ne = 0, nu = 0;
     bool chg = false, ovf = false;
 
@@ -210,18 +338,15 @@ __global__ void __launch_bounds__(B) k_expand(Args a) {
             const uint32_t idx = i0 + j;
             deg[j] = 0; beg[j] = 0; pay[j] = 0; uu[j] = 0;
             if (idx < nitems) {
-                const uint32_t u = implicit ? idx : in[idx];
+                const uint32_t u = implicit ? idx : ld_stream(in + idx, pf);
                 uu[j] = u;
-                bool act;
+                bool act = true;
                 uint32_t p = 0;
                 if (ALGO == SSSP) {
-                    act = STYLE == WORKLIST || a.stamp[u] == iter - 1;
-                    if (act) { p = (uint32_t)a.val[u]; act = p != (uint32_t)INF; }
-                } else if (ALGO == BFS) {
-                    act = STYLE == WORKLIST || a.val[u] == (int32_t)lev;
-                } else {
-                    act = true;
-                    p = (uint32_t)a.val[u];   // root label after the previous compress
+                    p = (uint32_t)ld_val(a.val + u, pl);
+                    act = p != (uint32_t)INF;
+                } else if (ALGO == CC) {
+                    p = (uint32_t)ld_val(a.val + u, pl);   // root label after the previous compress
                 }
                 if (act) {
                     const uint32_t b0 = ld_ro(a.row_off + u), b1 = ld_ro(a.row_off + u + 1);
@@ -268,152 +393,385 @@ __global__ void __launch_bounds__(B) k_expand(Args a) {
             for (int q = 0; q < U; q++) {
                 v[q] = 0; wt[q] = 0;
                 if (ok[q]) {
-                    v[q] = ld_stream(a.col + e[q]);
-                    if (ALGO == SSSP) wt[q] = ld_stream(a.w + e[q]);
+                    v[q] = ld_stream(a.col + e[q], pf);
+                    if (ALGO == SSSP) wt[q] = ld_stream(a.w + e[q], pf);
                 }
             }
             int32_t cur[U];
 #pragma unroll
-            for (int q = 0; q < U; q++) cur[q] = ok[q] ? a.val[v[q]] : 0;
+            for (int q = 0; q < U; q++) {
+                cur[q] = 0;
+                if (ok[q]) {
+                    if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;   // visited filter
+                    else cur[q] = ld_val(a.val + v[q], pl);
+                }
+            }
+            // Phased so that the U arcs' dependent round trips overlap:
+            // (D) the atomics whose old value decides the outcome, (E) the
+            // bitmap claims, (F) the queue pushes.
+            int32_t old[U];
+            uint32_t key[U];   // SSSP: cand; CC: lo; BFS: unused
+            bool tried[U];
 #pragma unroll
             for (int q = 0; q < U; q++) {
-                bool want = false;
-                uint32_t item = 0;
-                if (ok[q]) {
-                    if (ALGO == SSSP) {
-                        const uint32_t cand = s_pay[it[q]] + (uint32_t)wt[q];
-                        if (cand >= (uint32_t)INF) {
-                            ovf = true;
-                        } else if ((int32_t)cand < cur[q]) {
-                            const int32_t old = atomicMin(a.val + v[q], (int32_t)cand);
-                            if ((int32_t)cand < old) {
-                                nu++;
-                                if (STYLE == WORKLIST) {
-                                    if (a.stamp[v[q]] != iter && atomicExch(a.stamp + v[q], iter) != iter) {
-                                        want = true; item = v[q];
-                                    }
-                                } else {
-                                    a.stamp[v[q]] = iter;
-                                    chg = true;
-                                }
-                            }
-                        }
-                    } else if (ALGO == BFS) {
-                        if (STYLE == WORKLIST) {
-                            if (cur[q] == INF && atomicCAS(a.val + v[q], INF, (int32_t)(lev + 1)) == INF) {
-                                nu++; want = true; item = v[q];
-                            }
-                        } else if (cur[q] > (int32_t)(lev + 1)) {   // PAPER.md:1308-1310, plain store
-                            a.val[v[q]] = (int32_t)(lev + 1);
-                            nu++; chg = true;
-                        }
-                    } else {   // CC: hook the larger root under the smaller (min-label)
-                        const uint32_t lu = s_pay[it[q]], lv = (uint32_t)cur[q];
-                        if (lu != lv) {
-                            const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                            const int32_t old = atomicMin(a.val + hi, (int32_t)lo);
-                            if ((int32_t)lo < old) { nu++; chg = true; }
-                            if (STYLE == WORKLIST) {   // keep u while one of its arcs is unresolved
-                                const uint32_t u = s_u[it[q]];
-                                if (a.stamp[u] != iter && atomicExch(a.stamp + u, iter) != iter) {
-                                    want = true; item = u;
-                                }
-                            }
-                        }
+                tried[q] = false; old[q] = 0; key[q] = 0;
+                if (!ok[q]) continue;
+                if (ALGO == SSSP) {
+                    const uint32_t cand = s_pay[it[q]] + (uint32_t)wt[q];
+                    key[q] = cand;
+                    if (cand >= (uint32_t)INF) {
+                        ovf = true;
+                    } else if ((int32_t)cand < cur[q]) {
+                        old[q] = atomicMin(a.val + v[q], (int32_t)cand);
+                        tried[q] = true;
+                    }
+                } else if (ALGO == BFS) {
+                    // t.dist > lev+1 -> t.dist = lev+1; the visited
+                    // claim makes the store (and the append) happen exactly once
+                    if (cur[q] == INF) {
+                        old[q] = (int32_t)atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
+                        tried[q] = true;
+                    }
+                } else {   // CC: hook the larger root under the smaller (min-label)
+                    const uint32_t lu = s_pay[it[q]], lv = (uint32_t)cur[q];
+                    if (lu != lv) {
+                        const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
+                        key[q] = lo;
+                        old[q] = atomicMin(a.val + hi, (int32_t)lo);
+                        tried[q] = true;
                     }
                 }
-                if (STYLE == WORKLIST) warp_append(want, item, out, &c->out_len);
             }
+            bool need[U];
+            uint32_t citem[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                need[q] = false; citem[q] = 0;
+                if (!tried[q]) continue;
+                if (ALGO == SSSP) {
+                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; need[q] = true; citem[q] = v[q]; }
+                } else if (ALGO == BFS) {
+                    if (!((uint32_t)old[q] & (1u << (v[q] & 31)))) {
+                        a.val[v[q]] = (int32_t)(lev + 1);
+                        nu++; chg = true;
+                        if (STYLE == WORKLIST) { need[q] = true; citem[q] = v[q]; }
+                        else atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
+                    }
+                } else {
+                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; }
+                    if (STYLE == WORKLIST) { need[q] = true; citem[q] = s_u[it[q]]; }   // keep u while unresolved
+                }
+            }
+            uint32_t got[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                got[q] = 0xffffffffu;
+                if (!need[q]) continue;
+                if (ALGO == BFS) { got[q] = 0; continue; }   // the visited claim was the dedup
+                const uint32_t b = 1u << (citem[q] & 31);
+                if (STYLE == WORKLIST) got[q] = atomicOr(bm_now + (citem[q] >> 5), b);
+                else atomicOr(bm_now + (citem[q] >> 5), b);   // no return value: a reduction
+            }
+            if (STYLE == WORKLIST) {
+#pragma unroll
+                for (int q = 0; q < U; q++)
+                    bq.push(need[q] && !(got[q] & (1u << (citem[q] & 31))), citem[q]);
+            }
+            if (STYLE == WORKLIST) bq.flush(out, &c->out_len, QCAP > B * U ? QCAP - B * U : 0);
         }
         __syncthreads();
     }
+    if (STYLE == WORKLIST) bq.flush(out, &c->out_len, 0);
+    flush_counters<B>(a, nv, ne, nu, chg, ovf);
+}
+
+// ------------------------------------------------------------------ warp-centric expansion
+// Same work as k_expand, but a WARP owns 32 items: a shuffle scan turns their
+// degrees into offsets and the warp walks the concatenated arc ranges 32*U
+// arcs at a time, each lane finding its item by a 5-step shuffle binary
+// search.  No block barrier anywhere in the loop, so warps drift freely and
+// keep many independent gathers in flight (the path is latency / sector
+// bound: tools/l2probe.cu).  Appends go to a per-warp shared
+// queue flushed with one global atomicAdd per WQ - 32*U items.
+template <int ALGO, int STYLE, int B, int U, int MINB>
+__global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
+    static_assert(STYLE == VERTEX || STYLE == WORKLIST, "expand is for VERTEX/WORKLIST");
+    constexpr int NW = B / 32;
+    constexpr int WQ = STYLE == WORKLIST ? 512 : 1;
+    Ctrl *c = a.ctrl;
+    if (c->done) return;
+    const uint32_t iter = c->iter;
+    const uint32_t lev = iter - 1;
+    const uint32_t *in = c->sel ? a.fr1 : a.fr0;
+    uint32_t *out = c->sel ? a.fr0 : a.fr1;
+    const bool implicit = ALGO == CC && (STYLE == VERTEX || c->all_active != 0);
+    const uint32_t nitems = implicit ? a.n : c->in_len;
+    uint32_t *bm_now = bm_of(a, iter);
+    if (STYLE == WORKLIST || ALGO == CC) clear_next_bitmap(a, iter);
+    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
+
+    __shared__ uint32_t s_q[NW][WQ];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *wq = s_q[wid];
+    uint32_t qn = 0;   // warp-uniform count of staged appends
+    unsigned long long nv = 0, ne = 0, nu = 0;
+    bool chg = false, ovf = false;
+    const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
+
+    auto wflush = [&](uint32_t thresh) {
+        if (qn > thresh) {
+            uint32_t b = 0;
+            if (lane == 0) b = atomicAdd(&c->out_len, qn);
+            b = __shfl_sync(FULL, b, 0);
+            __syncwarp();
+            for (uint32_t i = lane; i < qn; i += 32) out[b + i] = wq[i];
+            __syncwarp();
+            qn = 0;
+        }
+    };
+
+    for (uint32_t wb = gw * 32; wb < nitems; wb += nwarps * 32) {   // warp-uniform
+        const uint32_t idx = wb + lane;
+        uint32_t u = 0, deg = 0, beg = 0, pay = 0;
+        if (idx < nitems) {
+            u = implicit ? idx : ld_stream(in + idx, pf);
+            bool act = true;
+            if (ALGO != BFS) {
+                pay = (uint32_t)ld_val(a.val + u, pl);
+                if (ALGO == SSSP) act = pay != (uint32_t)INF;
+            }
+            if (act) {
+                beg = ld_ro(a.row_off + u);
+                deg = ld_ro(a.row_off + u + 1) - beg;
+                nv++;
+            }
+        }
+        uint32_t incl = deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        const uint32_t excl = incl - deg;
+        if (lane == 0) ne += total;
+
+        for (uint32_t base = 0; base < total; base += 32 * U) {
+            uint32_t e[U], v[U], p[U], uj[U];
+            int32_t wt[U], cur[U];
+            bool ok[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                const uint32_t k = base + q * 32 + lane;
+                ok[q] = k < total;
+                int j = 0;
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) {
+                    const uint32_t ex = __shfl_sync(FULL, excl, j + st);
+                    if (ex <= k) j += st;
+                }
+                const uint32_t bj = __shfl_sync(FULL, beg, j), xj = __shfl_sync(FULL, excl, j);
+                p[q] = __shfl_sync(FULL, pay, j);
+                uj[q] = __shfl_sync(FULL, u, j);
+                e[q] = bj + (k - xj);
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                v[q] = 0; wt[q] = 0;
+                if (ok[q]) {
+                    v[q] = ld_stream(a.col + e[q], pf);
+                    if (ALGO == SSSP) wt[q] = ld_stream(a.w + e[q], pf);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                cur[q] = 0;
+                if (ok[q]) {
+                    if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;
+                    else cur[q] = ld_val(a.val + v[q], pl);
+                }
+            }
+            int32_t old[U];
+            uint32_t key[U];
+            bool tried[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                tried[q] = false; old[q] = 0; key[q] = 0;
+                if (!ok[q]) continue;
+                if (ALGO == SSSP) {
+                    const uint32_t cand = p[q] + (uint32_t)wt[q];
+                    key[q] = cand;
+                    if (cand >= (uint32_t)INF) ovf = true;
+                    else if ((int32_t)cand < cur[q]) { old[q] = atomicMin(a.val + v[q], (int32_t)cand); tried[q] = true; }
+                } else if (ALGO == BFS) {
+                    if (cur[q] == INF) {
+                        old[q] = (int32_t)atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
+                        tried[q] = true;
+                    }
+                } else {
+                    const uint32_t lu = p[q], lv = (uint32_t)cur[q];
+                    if (lu != lv) {
+                        const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
+                        key[q] = lo;
+                        old[q] = atomicMin(a.val + hi, (int32_t)lo);
+                        tried[q] = true;
+                    }
+                }
+            }
+            bool need[U];
+            uint32_t citem[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                need[q] = false; citem[q] = 0;
+                if (!tried[q]) continue;
+                if (ALGO == SSSP) {
+                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; need[q] = true; citem[q] = v[q]; }
+                } else if (ALGO == BFS) {
+                    if (!((uint32_t)old[q] & (1u << (v[q] & 31)))) {
+                        a.val[v[q]] = (int32_t)(lev + 1);
+                        nu++; chg = true;
+                        if (STYLE == WORKLIST) { need[q] = true; citem[q] = v[q]; }
+                        else atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
+                    }
+                } else {
+                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; }
+                    if (STYLE == WORKLIST) { need[q] = true; citem[q] = uj[q]; }
+                }
+            }
+            uint32_t got[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                got[q] = 0xffffffffu;
+                if (!need[q]) continue;
+                if (ALGO == BFS) { got[q] = 0; continue; }
+                const uint32_t b = 1u << (citem[q] & 31);
+                if (STYLE == WORKLIST) got[q] = atomicOr(bm_now + (citem[q] >> 5), b);
+                else atomicOr(bm_now + (citem[q] >> 5), b);
+            }
+            if (STYLE == WORKLIST) {
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
+                    const unsigned mask = __ballot_sync(FULL, want);
+                    if (want) wq[qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
+                    qn += __popc(mask);
+                }
+                __syncwarp();
+                wflush(WQ > 32 * U ? WQ - 32 * U : 0);
+            }
+        }
+    }
+    if (STYLE == WORKLIST) { __syncwarp(); wflush(0); }
     flush_counters<B>(a, nv, ne, nu, chg, ovf);
 }
 
 // ------------------------------------------------------------------ EDGE style (COO)
 // Four CSR-ordered arcs per thread per step through 16-byte loads of src,
-// col and w; col/w are only fetched when one of the four sources is active.
+// col and w; the source's activity bit (bm[(r-1)%3], L1/L2-resident) decides
+// whether col/w are fetched at all.
 template <int ALGO, int B>
 __global__ void __launch_bounds__(B) k_edge(Args a) {
     Ctrl *c = a.ctrl;
     if (c->done) return;
     const uint32_t iter = c->iter, lev = iter - 1;
+    clear_next_bitmap(a, iter);
+    const uint32_t *bm_prev = bm_of(a, iter - 1);
+    uint32_t *bm_now = bm_of(a, iter);
+    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
     const uint32_t m4 = a.m >> 2, tail = a.m & 3u;
-    unsigned long long nv = 0, ne = 0, nu = 0;
+    const uint32_t nq = m4 + (tail ? 1u : 0u);
+    unsigned long long ne = 0, nu = 0;
     bool chg = false, ovf = false;
-    const uint32_t stride = gridDim.x * B;
-    for (uint32_t q = blockIdx.x * B + threadIdx.x; q < m4 + (tail ? 1u : 0u); q += stride) {
+    for (uint32_t q = blockIdx.x * B + threadIdx.x; q < nq; q += gridDim.x * B) {
         const uint32_t cntq = q < m4 ? 4u : tail;
-        uint32_t s[4] = {0, 0, 0, 0}, d[4] = {0, 0, 0, 0};
+        uint32_t s[4] = {0, 0, 0, 0}, d[4] = {0, 0, 0, 0}, pay[4] = {0, 0, 0, 0};
         int32_t ww[4] = {0, 0, 0, 0};
         if (q < m4) {
-            const uint4 s4 = ld_stream4(a.src + 4ull * q);
+            const uint4 s4 = ld_stream4(a.src + 4ull * q, pf);
             s[0] = s4.x; s[1] = s4.y; s[2] = s4.z; s[3] = s4.w;
         } else {
-            for (uint32_t j = 0; j < cntq; j++) s[j] = ld_stream(a.src + 4ull * q + j);
+            for (uint32_t j = 0; j < cntq; j++) s[j] = ld_stream(a.src + 4ull * q + j, pf);
         }
         bool act[4];
-        uint32_t pay[4];
         bool any = false;
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            act[j] = false; pay[j] = 0;
-            if ((uint32_t)j < cntq) {
-                if (ALGO == SSSP) {
-                    // consecutive arcs share a source: these gathers hit L1
-                    act[j] = a.stamp[s[j]] == iter - 1;
-                    if (act[j]) { pay[j] = (uint32_t)a.val[s[j]]; act[j] = pay[j] != (uint32_t)INF; }
-                } else if (ALGO == BFS) {
-                    act[j] = a.val[s[j]] == (int32_t)lev;   // e.src.dist == lev (R14)
-                } else {
-                    act[j] = true; pay[j] = (uint32_t)a.val[s[j]];
-                }
-                any |= act[j];
-            }
+            // ALGO == CC: every arc hooks; otherwise the source must be active
+            act[j] = (uint32_t)j < cntq && (ALGO == CC || bit_test(bm_prev, s[j]));
+            any |= act[j];
         }
         if (!any) continue;
         if (q < m4) {
-            const uint4 d4 = ld_stream4(a.col + 4ull * q);
+            const uint4 d4 = ld_stream4(a.col + 4ull * q, pf);
             d[0] = d4.x; d[1] = d4.y; d[2] = d4.z; d[3] = d4.w;
             if (ALGO == SSSP) {
-                const int4 w4 = ld_stream4(a.w + 4ull * q);
+                const int4 w4 = ld_stream4(a.w + 4ull * q, pf);
                 ww[0] = w4.x; ww[1] = w4.y; ww[2] = w4.z; ww[3] = w4.w;
             }
         } else {
             for (uint32_t j = 0; j < cntq; j++) {
-                d[j] = ld_stream(a.col + 4ull * q + j);
-                if (ALGO == SSSP) ww[j] = ld_stream(a.w + 4ull * q + j);
+                d[j] = ld_stream(a.col + 4ull * q + j, pf);
+                if (ALGO == SSSP) ww[j] = ld_stream(a.w + 4ull * q + j, pf);
             }
         }
         int32_t cur[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) cur[j] = act[j] ? a.val[d[j]] : 0;
+        for (int j = 0; j < 4; j++) {
+            cur[j] = 0;
+            if (!act[j]) continue;
+            if (ALGO != BFS) pay[j] = (uint32_t)ld_val(a.val + s[j], pl);   // consecutive arcs share a source
+            if (ALGO == BFS) cur[j] = bit_test(a.vis, d[j]) ? 0 : INF;
+            else cur[j] = ld_val(a.val + d[j], pl);
+        }
+        // phased like k_expand: all four atomics in flight before any result is used
+        int32_t old[4];
+        uint32_t key[4];
+        bool tried[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
+            tried[j] = false; old[j] = 0; key[j] = 0;
             if (!act[j]) continue;
             ne++;
             if (ALGO == SSSP) {
                 const uint32_t cand = pay[j] + (uint32_t)ww[j];
+                key[j] = cand;
                 if (cand >= (uint32_t)INF) { ovf = true; continue; }
-                if ((int32_t)cand < cur[j]) {
-                    const int32_t old = atomicMin(a.val + d[j], (int32_t)cand);
-                    if ((int32_t)cand < old) { a.stamp[d[j]] = iter; nu++; chg = true; }
+                if ((int32_t)cand < cur[j]) { old[j] = atomicMin(a.val + d[j], (int32_t)cand); tried[j] = true; }
+            } else if (ALGO == BFS) {   // e.src.dist == lev (R14) via the bitmap
+                if (cur[j] == INF) {
+                    old[j] = (int32_t)atomicOr(a.vis + (d[j] >> 5), 1u << (d[j] & 31));
+                    tried[j] = true;
                 }
-            } else if (ALGO == BFS) {
-                if (cur[j] > (int32_t)(lev + 1)) { a.val[d[j]] = (int32_t)(lev + 1); nu++; chg = true; }
             } else {
                 const uint32_t lu = pay[j], lv = (uint32_t)cur[j];
                 if (lu != lv) {
                     const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                    const int32_t old = atomicMin(a.val + hi, (int32_t)lo);
-                    if ((int32_t)lo < old) { nu++; chg = true; }
+                    key[j] = lo;
+                    old[j] = atomicMin(a.val + hi, (int32_t)lo);
+                    tried[j] = true;
                 }
             }
         }
-        if (ALGO != SSSP) (void)ww;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (!tried[j]) continue;
+            if (ALGO == SSSP) {
+                if ((int32_t)key[j] < old[j]) {
+                    atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
+                    nu++; chg = true;
+                }
+            } else if (ALGO == BFS) {
+                if (!((uint32_t)old[j] & (1u << (d[j] & 31)))) {
+                    a.val[d[j]] = (int32_t)(lev + 1);
+                    atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
+                    nu++; chg = true;
+                }
+            } else {
+                if ((int32_t)key[j] < old[j]) { nu++; chg = true; }
+            }
+        }
     }
-    // vertices processed: count arcs' distinct sources is not tracked in EDGE style
-    flush_counters<B>(a, nv, ne, nu, chg, ovf);
+    flush_counters<B>(a, 0ull, ne, nu, chg, ovf);
 }
 
 // ------------------------------------------------------------------ CC pointer jumping
@@ -454,6 +812,8 @@ __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, u
             c->out_len = 0;
             c->sel ^= 1u;
             c->all_active = 0;
+        } else if (STYLE == VERTEX) {
+            c->in_len = 0;   // k_scan rebuilds the frontier of the next round
         }
     } else {
         c->done = 1;
