@@ -29,6 +29,7 @@ constexpr int BLOCK = 256;
 constexpr int IPT_ALL = 4;  // items per thread per tile when every vertex is an item (CC VERTEX)
 constexpr int IPT_FR = 1;   // frontier items per thread per tile
 constexpr int UNROLL = 4;   // arcs per thread per expansion step
+constexpr int EDGE_QP = 4;   // 4-arc quads per thread per step (EDGE style)
 constexpr int MINB = 4;     // min resident CTAs per SM for the warp-centric expansion
 constexpr int HOST_CHECK_EVERY = 4;
 
@@ -71,6 +72,9 @@ struct falcon_graph {
     int64_t n = 0, m = 0;
     uint32_t *row_off = nullptr, *col = nullptr, *src = nullptr;
     int32_t *w = nullptr;
+    uint2 *cw = nullptr;
+    uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
+    uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     int32_t *val = nullptr;
     uint32_t *bm = nullptr, *fr0 = nullptr, *fr1 = nullptr;   // bm: 4 bitmaps of nwords
     uint32_t nwords = 0;
@@ -79,12 +83,13 @@ struct falcon_graph {
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_expand_all = 0, grid_expand_fr = 0, grid_scan = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    int grid_expand_all = 0, grid_expand_fr = 0, grid_scan = 0, grid_pull = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
     cudaGraph_t graphs[3][3] = {};
     cudaGraphExec_t execs[3][3] = {};
     bool profiling = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> pev;
+    int variant = 0;                     // FALCON_EXPAND_VARIANT
     bool warp_expand = true;             // warp-centric expansion (FALCON_EXPAND=cta for the CTA-tile kernel)
     bool l2_window = false;              // persisting L2 access-policy window on val[]
     cudaAccessPolicyWindow apw = {};
@@ -92,7 +97,8 @@ struct falcon_graph {
     Args args() const {
         Args a;
         a.n = (uint32_t)n; a.m = (uint32_t)m; a.nwords = nwords;
-        a.row_off = row_off; a.col = col; a.w = w; a.src = src;
+        a.row_off = row_off; a.col = col; a.w = w; a.cw = cw; a.src = src;
+        a.rin_off = rin_off; a.rin_col = rin_col;
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
@@ -122,44 +128,89 @@ void launch_l2(const falcon_graph *g, void (*k)(KArgs...), int grid, cudaStream_
     cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...);
 }
 
+// Profiling / tracing: an event after every launch of a round (host-driven
+// loop only).  Kinds: 0 = relax kernel (scan, expand, edge), 1 = other.
+struct Tracer {
+    falcon_graph *g;
+    size_t next = 0;
+    struct Mark { cudaEvent_t ev; const char *name; int kind; uint32_t round; };
+    std::vector<Mark> marks;
+    uint32_t round = 0;
+    void mark(cudaStream_t s, const char *name, int kind);
+};
+
+// Expansion-kernel variants (arcs per lane per step U, min resident CTAs per
+// SM): selected at load time by FALCON_EXPAND_VARIANT (tuning experiments).
+template <int ALGO, int STYLE>
+void launch_expand_warp(const falcon_graph *g, cudaStream_t s, const Args &a) {
+    switch (g->variant) {
+    case 1: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 8>, g->grid_expand_fr, s, a); break;
+    case 2: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 2>, g->grid_expand_fr, s, a); break;
+    case 3: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 3>, g->grid_expand_fr, s, a); break;
+    case 4: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 6>, g->grid_expand_fr, s, a); break;
+    default: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a); break;
+    }
+}
+
 template <int ALGO, int STYLE>
 struct Round {
     // Launch one round's kernels on `s`.  Returns the number of launches.
-    static int launch(falcon_graph *g, cudaStream_t s, cudaGraphConditionalHandle h, int in_graph,
-                      std::vector<cudaEvent_t> *ev) {
+    static int launch(falcon_graph *g, cudaStream_t s, cudaGraphConditionalHandle h, int in_graph, Tracer *tr) {
         Args a = g->args();
         int launches = 0;
-        if (ev) cudaEventRecord((*ev)[0], s);
+        if (tr) tr->mark(s, "begin", 1);
         if (STYLE == VERTEX && ALGO == CC) {
-            if (g->warp_expand) launch_l2(g, k_expand_warp<ALGO, VERTEX, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a);
+            if (g->warp_expand) launch_expand_warp<ALGO, VERTEX>(g, s, a);
             else launch_l2(g, k_expand<ALGO, VERTEX, BLOCK, IPT_ALL, UNROLL>, g->grid_expand_all, s, a);
+            if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == VERTEX) {
-            launch_l2(g, k_scan<BLOCK>, g->grid_scan, s, a);
+            launch_l2(g, k_scan<ALGO, BLOCK>, g->grid_scan, s, a);
             launches++;
-            if (g->warp_expand) launch_l2(g, k_expand_warp<ALGO, VERTEX, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a);
+            if (tr) tr->mark(s, "scan", 0);
+            if (ALGO == BFS) {
+                launch_l2(g, k_pull<BLOCK>, g->grid_pull, s, a);
+                launches++;
+                if (tr) tr->mark(s, "pull", 0);
+            }
+            if (g->warp_expand) launch_expand_warp<ALGO, VERTEX>(g, s, a);
             else launch_l2(g, k_expand<ALGO, VERTEX, BLOCK, IPT_FR, UNROLL>, g->grid_expand_fr, s, a);
+            if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == WORKLIST) {
-            if (g->warp_expand) launch_l2(g, k_expand_warp<ALGO, WORKLIST, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a);
+            if (g->warp_expand) launch_expand_warp<ALGO, WORKLIST>(g, s, a);
             else launch_l2(g, k_expand<ALGO, WORKLIST, BLOCK, IPT_FR, UNROLL>, g->grid_expand_fr, s, a);
+            if (tr) tr->mark(s, "expand", 0);
         } else {
-            launch_l2(g, k_edge<ALGO, BLOCK>, g->grid_edge, s, a);
+            launch_l2(g, k_edge<ALGO, BLOCK, EDGE_QP>, g->grid_edge, s, a);
+            if (tr) tr->mark(s, "edge", 0);
         }
         launches++;
-        if (ev) cudaEventRecord((*ev)[1], s);
         if (ALGO == CC) {
             launch_l2(g, k_compress, g->grid_small, s, a);
             launches++;
+            if (tr) tr->mark(s, "compress", 1);
         }
         launches++;
-        k_advance<STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches);
+        k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n, g->pull_div);
+        if (tr) tr->mark(s, "advance", 1);
         return launches;
     }
 };
 
+void Tracer::mark(cudaStream_t s, const char *name, int kind) {
+    while (g->pev.size() <= next) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        g->pev.push_back(e);
+    }
+    cudaEvent_t e = g->pev[next++];
+    cudaEventRecord(e, s);
+    marks.push_back({e, name, kind, round});
+}
+
 int launch_round(falcon_graph *g, int algo, int style, cudaStream_t s, cudaGraphConditionalHandle h, int in_graph,
-                 std::vector<cudaEvent_t> *ev) {
+                 Tracer *tr) {
 #define R(A, S) \
-    if (algo == A && style == S) return Round<A, S>::launch(g, s, h, in_graph, ev);
+    if (algo == A && style == S) return Round<A, S>::launch(g, s, h, in_graph, tr);
     R(SSSP, VERTEX) R(SSSP, EDGE) R(SSSP, WORKLIST)
     R(BFS, VERTEX) R(BFS, EDGE) R(BFS, WORKLIST)
     R(CC, VERTEX) R(CC, EDGE) R(CC, WORKLIST)
@@ -211,6 +262,31 @@ falcon_status_t ensure_src(falcon_graph *g) {
     return FALCON_OK;
 }
 
+// Reverse CSR for bottom-up BFS (built once, on the device).
+falcon_status_t ensure_reverse(falcon_graph *g) {
+    if (g->rin_off) return FALCON_OK;
+    const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
+    cudaStream_t s = g->stream;
+    CU(dmalloc(&g->rin_off, n + 1));
+    CU(dmalloc(&g->rin_col, m));
+    uint32_t *cursor = nullptr, *tiles = nullptr;
+    const uint32_t ntiles = (uint32_t)((n + 1 + 1023) / 1024);
+    CU(dmalloc(&cursor, n + 1));
+    CU(dmalloc(&tiles, ntiles));
+    CU(cudaMemsetAsync(g->rin_off, 0, (n + 1) * 4, s));
+    if (m) k_indeg<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->col, g->rin_off);
+    k_scan_local<<<ntiles, 256, 0, s>>>(g->rin_off, n + 1, tiles);
+    k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
+    k_scan_add<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(g->rin_off, n + 1, tiles);
+    CU(cudaMemcpyAsync(cursor, g->rin_off, (n + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    if (m) k_rev_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->col, cursor, g->rin_col);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s));
+    cudaFree(cursor);
+    cudaFree(tiles);
+    return FALCON_OK;
+}
+
 falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out, falcon_stats_t *stats) {
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
@@ -219,6 +295,10 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     CU(cudaSetDevice(g->device));
     if (style == EDGE) {
         falcon_status_t st = ensure_src(g);
+        if (st != FALCON_OK) return st;
+    }
+    if (algo == BFS && style == VERTEX && g->pull_div) {
+        falcon_status_t st = ensure_reverse(g);
         if (st != FALCON_OK) return st;
     }
     cudaStream_t s = g->stream;
@@ -237,34 +317,43 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
         if (st != FALCON_OK) return st;
         CU(cudaGraphLaunch(g->execs[algo][style], s));
     } else {
-        // Host-driven loop with CUDA events around every relax launch.
-        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pairs;
-        size_t next_ev = 0;
+        // Host-driven loop with a CUDA event after every launch (same kernels).
+        const char *trace_env = getenv("FALCON_TRACE");
+        const bool trace = trace_env && trace_env[0] == '1';
+        Tracer tr{g};
+        std::vector<uint32_t> fr_len;   // trace: frontier length after each round
         for (;;) {
-            for (int k = 0; k < HOST_CHECK_EVERY; k++) {
-                while (g->pev.size() < next_ev + 2) {
-                    cudaEvent_t e;
-                    CU(cudaEventCreate(&e));
-                    g->pev.push_back(e);
-                }
-                std::vector<cudaEvent_t> ev = {g->pev[next_ev], g->pev[next_ev + 1]};
-                pairs.push_back({ev[0], ev[1]});
-                next_ev += 2;
-                launch_round(g, algo, style, s, 0, 0, &ev);
+            const int per_check = trace ? 1 : HOST_CHECK_EVERY;
+            for (int k = 0; k < per_check; k++) {
+                tr.round++;
+                launch_round(g, algo, style, s, 0, 0, &tr);
             }
             CU(cudaGetLastError());
             CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
             CU(cudaStreamSynchronize(s));
+            if (trace) fr_len.push_back(g->h_ctrl->in_len);
             if (g->h_ctrl->done) break;
         }
         const uint32_t rounds = g->h_ctrl->iter;
         relax_ms = 0.0;
-        for (size_t i = 0; i < pairs.size() && i < rounds; i++) {
+        std::vector<std::string> lines;
+        for (size_t i = 1; i < tr.marks.size(); i++) {
+            const auto &m = tr.marks[i];
+            if (m.round > rounds || std::strcmp(m.name, "begin") == 0) continue;
             float t = 0.f;
-            CU(cudaEventElapsedTime(&t, pairs[i].first, pairs[i].second));
-            relax_ms += t;
-            relax_launches++;
+            CU(cudaEventElapsedTime(&t, tr.marks[i - 1].ev, m.ev));
+            if (m.kind == 0) relax_ms += t;
+            if (std::strcmp(m.name, "expand") == 0 || std::strcmp(m.name, "edge") == 0) relax_launches++;
+            if (trace) {
+                char buf[160];
+                snprintf(buf, sizeof buf, "round %4u %-9s %9.1f us%s", m.round, m.name, 1e3 * t,
+                         std::strcmp(m.name, "advance") == 0 && m.round - 1 < fr_len.size()
+                             ? (" | frontier after round: " + std::to_string(fr_len[m.round - 1])).c_str() : "");
+                lines.push_back(buf);
+            }
         }
+        if (trace)
+            for (auto &l : lines) fprintf(stderr, "[falcon trace] %s\n", l.c_str());
     }
     k_finish<<<1, BLOCK, 0, s>>>(a, (uint32_t)g->cnt_slots);
     CU(cudaGetLastError());
@@ -304,7 +393,8 @@ void destroy(falcon_graph *g) {
     for (auto e : g->pev) cudaEventDestroy(e);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
-    cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->src);
+    cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->cw); cudaFree(g->src);
+    cudaFree(g->rin_off); cudaFree(g->rin_col);
     cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1);
     cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
@@ -348,25 +438,33 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (m) CU(cudaMemcpyAsync(g->col, col, (size_t)m * 4, cudaMemcpyDefault, s));
     if (m && w) CU(cudaMemcpyAsync(g->w, w, (size_t)m * 4, cudaMemcpyDefault, s));
     if (m && !w) k_fill_i32<<<g->num_sms * 8, BLOCK, 0, s>>>(g->w, (uint64_t)m, 1);
+    CU(dmalloc(&g->cw, (size_t)m));
+    if (m) k_interleave<<<g->num_sms * 8, BLOCK, 0, s>>>((uint64_t)m, g->col, g->w, g->cw);
 
     // grid sizes: a multiple of the SM count x resident CTAs, capped by the work
     int occ_a = 0, occ_f = 0, occ_e = 0, occ_s = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_expand<CC, VERTEX, BLOCK, IPT_ALL, UNROLL>, BLOCK, 0));
     const char *ex = getenv("FALCON_EXPAND");
     g->warp_expand = !(ex && strcmp(ex, "cta") == 0);
+    const char *var = getenv("FALCON_EXPAND_VARIANT");
+    g->variant = var ? atoi(var) : 0;
+    static const int var_minb[5] = {MINB, 8, 2, 3, 6};
     if (g->warp_expand)
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_expand_warp<SSSP, WORKLIST, BLOCK, UNROLL, MINB>, BLOCK, 0));
+        occ_f = var_minb[g->variant >= 0 && g->variant < 5 ? g->variant : 0];
     else
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_expand<SSSP, WORKLIST, BLOCK, IPT_FR, UNROLL>, BLOCK, 0));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK>, BLOCK, 0));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scan<BLOCK>, BLOCK, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK, EDGE_QP>, BLOCK, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scan<SSSP, BLOCK>, BLOCK, 0));
     auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };
     auto full = [&](int occ) { return (int64_t)g->num_sms * (occ > 0 ? occ : 1); };
     g->grid_expand_all = clampg((n + BLOCK * IPT_ALL - 1) / (BLOCK * IPT_ALL), full(occ_a));
     g->grid_expand_fr = clampg((n + BLOCK * IPT_FR - 1) / (BLOCK * IPT_FR), full(occ_f));
-    g->grid_edge = clampg((m / 4 + 1 + BLOCK - 1) / BLOCK, full(occ_e));
-    g->grid_scan = clampg((g->nwords / 4 + BLOCK - 1) / BLOCK, full(occ_s));
+    g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP - 1) / (BLOCK * EDGE_QP), full(occ_e));
+    g->grid_scan = clampg((g->nwords + 4 * BLOCK - 1) / (4 * BLOCK), (int64_t)g->num_sms * 4);
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
+    g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
+    const char *pd = getenv("FALCON_BFS_PULL_DIV");
+    if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_expand_all;
     if (g->grid_expand_fr > slots) slots = g->grid_expand_fr;
     if (g->grid_edge > slots) slots = g->grid_edge;

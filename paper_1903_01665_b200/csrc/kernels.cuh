@@ -49,7 +49,8 @@ struct Ctrl {
     uint32_t all_active;  // CC round 1: frontier = all vertices (implicit)
     int32_t status;       // DevStatus
     uint32_t source;
-    uint32_t pad0, pad1;
+    uint32_t pull;        // BFS VERTEX: this round runs bottom-up (pull over in-arcs)
+    uint32_t found;       // BFS: vertices discovered this round (direction heuristic)
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
     unsigned long long edges;
@@ -61,7 +62,10 @@ struct Args {
     const uint32_t *row_off;   // [n+1]
     const uint32_t *col;       // [m]
     const int32_t *w;          // [m]
+    const uint2 *cw;           // [m] (col, w) interleaved: SSSP reads one 8-byte word per arc
     const uint32_t *src;       // [m] COO sources (CSR order), EDGE style only
+    const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
+    const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
     uint32_t *bm0, *bm1, *bm2; // round bitmaps [nwords] each
     uint32_t *vis;             // BFS visited bitmap [nwords]
@@ -109,6 +113,18 @@ __device__ __forceinline__ int4 ld_stream4(const int32_t *p, uint64_t pol) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ uint2 ld_stream2(const uint2 *p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_stream4(const uint2 *p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
 // mutable value array (written by atomics in the same kernel): coherent
 // load, evict-last so the gathered array stays L2-resident
 __device__ __forceinline__ int32_t ld_val(const int32_t *p, uint64_t pol) {
@@ -150,7 +166,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t &total,
 
 template <int B>
 __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long nv, unsigned long long ne,
-                                               unsigned long long nu, bool chg, bool ovf) {
+                                               unsigned long long nu, bool chg, bool ovf, bool count_found = false) {
     __shared__ unsigned long long s_red[3][B / 32];
     __shared__ int s_flags;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -171,6 +187,7 @@ __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long
         for (int i = 0; i < B / 32; i++) { t0 += s_red[0][i]; t1 += s_red[1][i]; t2 += s_red[2][i]; }
         unsigned long long *c = a.cnt + 3ull * blockIdx.x;   // this CTA's private slot: no atomics
         c[0] += t0; c[1] += t1; c[2] += t2;
+        if (count_found && t2) atomicAdd(&a.ctrl->found, (uint32_t)t2);
         if (s_flags & 1) a.ctrl->changed = 1;
         if (s_flags & 2) a.ctrl->status = ST_OVERFLOW;
     }
@@ -245,49 +262,132 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->all_active = ALGO == CC ? 1u : 0u;
         c->status = ST_OK; c->source = source;
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
+        c->pull = 0; c->found = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
 }
 
 // ------------------------------------------------------------------ VERTEX activity scan
 // Topology-driven round, part 1: visit EVERY vertex through
-// its bit in bm[(r-1)%3] and compact the active ones into the frontier, 128
-// vertices per thread per step (16-byte bitmap loads); one global atomicAdd
-// per CTA step.  Also clears bm[(r+1)%3].
-template <int B>
+// its bit in bm[(r-1)%3] and compact the active ones, in vertex order, into
+// the frontier.  Each CTA owns a contiguous range of bitmap words: pass 1
+// counts its set bits (one global atomicAdd per CTA per round), pass 2 writes
+// them warp-cooperatively (one ballot per word: coalesced stores).  Also
+// clears bm[(r+1)%3].
+template <int ALGO, int B>
 __global__ void __launch_bounds__(B) k_scan(Args a) {
+    constexpr int NW = B / 32;
     Ctrl *c = a.ctrl;
     if (c->done) return;
-    const uint32_t iter = c->iter;
+    const uint32_t iter = c->iter, lev = iter - 1;
     clear_next_bitmap(a, iter);
-    const uint4 *bm = reinterpret_cast<const uint4 *>(bm_of(a, iter - 1));
-    __shared__ uint32_t s_warp[B / 32];
+    // BFS: levels are written here, in vertex order, for the vertices the
+    // previous round discovered (bm[(r-1)%3]) -- dense sequential stores
+    // instead of one random store per discovery.  A pull round writes the
+    // levels but needs no compacted frontier.
+    const bool compact = !(ALGO == BFS && c->pull);
+    const uint32_t *bm = bm_of(a, iter - 1);
+    __shared__ uint32_t s_w[NW];
     __shared__ uint32_t s_base;
-    const uint32_t n4 = a.nwords >> 2;
-    for (uint32_t b0 = blockIdx.x * B; b0 < n4; b0 += gridDim.x * B) {   // block-uniform
-        const uint32_t i = b0 + threadIdx.x;
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (i < n4) x = bm[i];
-        const uint32_t cnt = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-        uint32_t total;
-        uint32_t off = block_excl_scan<B>(cnt, total, s_warp);
-        if (total == 0) continue;
-        if (threadIdx.x == 0) s_base = atomicAdd(&c->in_len, total);
-        __syncthreads();
-        off += s_base;
-        const uint32_t words[4] = {x.x, x.y, x.z, x.w};
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t per = ((a.nwords + gridDim.x - 1) / gridDim.x + B - 1) / B * B;
+    const uint32_t lo = blockIdx.x * per;
+    const uint32_t hi = lo + per < a.nwords ? lo + per : a.nwords;
+    uint32_t run = 0;
+    if (compact) {   // pass 1: count (block-uniform branch)
+        uint32_t cnt = 0;
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += B) cnt += __popc(bm[i]);
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            uint32_t wv = words[j];
-            const uint32_t vb = (4 * i + j) * 32;
-            while (wv) {
-                const int bpos = __ffs(wv) - 1;
-                wv &= wv - 1;
-                a.fr0[off++] = vb + bpos;   // bits beyond n are never set
-            }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+        if (lane == 0) s_w[wid] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int i = 0; i < NW; i++) t += s_w[i];
+            s_base = t ? atomicAdd(&c->in_len, t) : 0;
         }
         __syncthreads();
+        run = s_base;
+        __syncthreads();
     }
+    // pass 2: write, B words per CTA step, 32 words per warp
+    for (uint32_t i0 = lo; i0 < hi; i0 += B) {   // block-uniform
+        const uint32_t i = i0 + threadIdx.x;
+        const uint32_t w = i < hi ? bm[i] : 0u;
+        if (ALGO == BFS && w) {
+            uint32_t x = w;
+            while (x) {
+                const int bp = __ffs(x) - 1;
+                x &= x - 1;
+                a.val[i * 32u + bp] = (int32_t)lev;
+            }
+        }
+        if (!compact) continue;
+        uint32_t incl = __popc(w);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - __popc(w);
+        if (lane == 31) s_w[wid] = incl;
+        __syncthreads();
+        uint32_t wbase = run, tot = 0;
+        for (int k = 0; k < NW; k++) {
+            const uint32_t x = s_w[k];
+            if (k < wid) wbase += x;
+            tot += x;
+        }
+        __syncthreads();
+        run += tot;
+        const uint32_t wbeg = i0 + 32 * wid;
+        for (int j = 0; j < 32; j++) {   // warp-uniform
+            const uint32_t wj = __shfl_sync(FULL, w, j);
+            if (wj == 0) continue;
+            const uint32_t ej = __shfl_sync(FULL, excl, j);
+            if ((wj >> lane) & 1u)
+                a.fr0[wbase + ej + __popc(wj & ((1u << lane) - 1u))] = (wbeg + j) * 32u + lane;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ BFS bottom-up (pull) round
+// Direction-optimising BFS, VERTEX style over `innbrs` (Table
+// "Iterators"): every unvisited vertex scans its in-arcs until it finds a
+// parent in the previous level (bm[(r-1)%3]).  A warp owns one 32-vertex
+// bitmap word, so the visited / next-frontier words are written with plain
+// stores.  Run when the frontier is large (k_advance).
+template <int B>
+__global__ void __launch_bounds__(B) k_pull(Args a) {
+    Ctrl *c = a.ctrl;
+    if (c->done || !c->pull) return;
+    const uint32_t iter = c->iter;
+    const uint32_t *bm_prev = bm_of(a, iter - 1);
+    uint32_t *bm_now = bm_of(a, iter);
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
+    unsigned long long nv = 0, ne = 0, nu = 0;
+    bool chg = false;
+    for (uint32_t wi = gw; wi < a.nwords; wi += nwarps) {
+        const uint32_t visw = a.vis[wi];
+        const uint32_t v = wi * 32u + lane;
+        bool found = false;
+        if (v < a.n && !((visw >> lane) & 1u)) {
+            nv++;
+            const uint32_t e1 = ld_ro(a.rin_off + v + 1);
+            for (uint32_t e = ld_ro(a.rin_off + v); e < e1; e++) {
+                ne++;
+                if (bit_test(bm_prev, ld_ro(a.rin_col + e))) { found = true; break; }
+            }
+        }
+        const unsigned mask = __ballot_sync(FULL, found);
+        if (mask && lane == 0) {
+            a.vis[wi] = visw | mask;
+            bm_now[wi] = mask;
+        }
+        if (found) { nu++; chg = true; }
+    }
+    flush_counters<B>(a, nv, ne, nu, chg, false, true);
 }
 
 // ------------------------------------------------------------------ expansion (VERTEX / WORKLIST)
@@ -393,8 +493,12 @@ __global__ void __launch_bounds__(B, 4) k_expand(Args a) {
             for (int q = 0; q < U; q++) {
                 v[q] = 0; wt[q] = 0;
                 if (ok[q]) {
-                    v[q] = ld_stream(a.col + e[q], pf);
-                    if (ALGO == SSSP) wt[q] = ld_stream(a.w + e[q], pf);
+                    if (ALGO == SSSP) {   // one 8-byte (col, w) word: one DRAM burst per row
+                        const uint2 x = ld_stream2(a.cw + e[q], pf);
+                        v[q] = x.x; wt[q] = (int32_t)x.y;
+                    } else {
+                        v[q] = ld_stream(a.col + e[q], pf);
+                    }
                 }
             }
             int32_t cur[U];
@@ -489,17 +593,24 @@ __global__ void __launch_bounds__(B, 4) k_expand(Args a) {
 // Same work as k_expand, but a WARP owns 32 items: a shuffle scan turns their
 // degrees into offsets and the warp walks the concatenated arc ranges 32*U
 // arcs at a time, each lane finding its item by a 5-step shuffle binary
-// search.  No block barrier anywhere in the loop, so warps drift freely and
-// keep many independent gathers in flight (the path is latency / sector
-// bound: tools/l2probe.cu).  Appends go to a per-warp shared
-// queue flushed with one global atomicAdd per WQ - 32*U items.
+// search.  No block barrier in the loop, so warps drift freely.  The path is
+// bound by the latency of dependent memory round trips, so:
+//  * item loads are software-pipelined two tiles ahead (frontier entry two
+//    tiles ahead, value / row offsets one tile ahead);
+//  * VERTEX relaxations are fire-and-forget: the read filter `cand < val[v]`
+//    decides, atomicMin / the bitmap OR are issued as reductions (RED) whose
+//    results nobody waits for.  A vertex whose read passed the filter is
+//    improved in this round -- by us, or by whoever lowered it further after
+//    our read, who marks it too -- so the marked set is exactly the set of
+//    vertices improved this round (R8);
+//  * WORKLIST needs the old bitmap word to append each vertex once.
 template <int ALGO, int STYLE, int B, int U, int MINB>
 __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     static_assert(STYLE == VERTEX || STYLE == WORKLIST, "expand is for VERTEX/WORKLIST");
     constexpr int NW = B / 32;
     constexpr int WQ = STYLE == WORKLIST ? 512 : 1;
     Ctrl *c = a.ctrl;
-    if (c->done) return;
+    if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull)) return;
     const uint32_t iter = c->iter;
     const uint32_t lev = iter - 1;
     const uint32_t *in = c->sel ? a.fr1 : a.fr0;
@@ -517,6 +628,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     unsigned long long nv = 0, ne = 0, nu = 0;
     bool chg = false, ovf = false;
     const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
+    const uint32_t wstride = nwarps * 32;
 
     auto wflush = [&](uint32_t thresh) {
         if (qn > thresh) {
@@ -529,23 +641,34 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
             qn = 0;
         }
     };
+    auto item_of = [&](uint32_t idx) -> uint32_t {
+        return idx < nitems ? (implicit ? idx : ld_stream(in + idx, pf)) : 0xffffffffu;
+    };
+    // software pipeline: u1 = item of the current tile, u2 = item of the next
+    // tile; pay1/beg1/end1 = value and row offsets of the current tile's item
+    uint32_t wb = gw * 32;
+    uint32_t u1 = item_of(wb + lane), u2 = item_of(wb + wstride + lane);
+    uint32_t pay1 = 0, beg1 = 0, end1 = 0;
+    if (u1 != 0xffffffffu) {
+        if (ALGO != BFS) pay1 = (uint32_t)ld_val(a.val + u1, pl);
+        beg1 = ld_ro(a.row_off + u1); end1 = ld_ro(a.row_off + u1 + 1);
+    }
 
-    for (uint32_t wb = gw * 32; wb < nitems; wb += nwarps * 32) {   // warp-uniform
-        const uint32_t idx = wb + lane;
-        uint32_t u = 0, deg = 0, beg = 0, pay = 0;
-        if (idx < nitems) {
-            u = implicit ? idx : ld_stream(in + idx, pf);
-            bool act = true;
-            if (ALGO != BFS) {
-                pay = (uint32_t)ld_val(a.val + u, pl);
-                if (ALGO == SSSP) act = pay != (uint32_t)INF;
-            }
-            if (act) {
-                beg = ld_ro(a.row_off + u);
-                deg = ld_ro(a.row_off + u + 1) - beg;
-                nv++;
-            }
+    for (; wb < nitems; wb += wstride) {   // warp-uniform
+        const uint32_t u = u1, pay = pay1;
+        uint32_t beg = beg1, deg = end1 - beg1;
+        // issue the pipeline's next loads before touching this tile's arcs
+        u1 = u2;
+        u2 = item_of(wb + 2 * wstride + lane);
+        if (u1 != 0xffffffffu) {
+            if (ALGO != BFS) pay1 = (uint32_t)ld_val(a.val + u1, pl);
+            beg1 = ld_ro(a.row_off + u1); end1 = ld_ro(a.row_off + u1 + 1);
+        } else {
+            pay1 = 0; beg1 = 0; end1 = 0;
         }
+        if (u == 0xffffffffu || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
+        else nv++;
+
         uint32_t incl = deg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -579,8 +702,12 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
             for (int q = 0; q < U; q++) {
                 v[q] = 0; wt[q] = 0;
                 if (ok[q]) {
-                    v[q] = ld_stream(a.col + e[q], pf);
-                    if (ALGO == SSSP) wt[q] = ld_stream(a.w + e[q], pf);
+                    if (ALGO == SSSP) {   // one 8-byte (col, w) word: one DRAM burst per row
+                        const uint2 x = ld_stream2(a.cw + e[q], pf);
+                        v[q] = x.x; wt[q] = (int32_t)x.y;
+                    } else {
+                        v[q] = ld_stream(a.col + e[q], pf);
+                    }
                 }
             }
 #pragma unroll
@@ -591,67 +718,61 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
                     else cur[q] = ld_val(a.val + v[q], pl);
                 }
             }
-            int32_t old[U];
-            uint32_t key[U];
-            bool tried[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                tried[q] = false; old[q] = 0; key[q] = 0;
-                if (!ok[q]) continue;
-                if (ALGO == SSSP) {
-                    const uint32_t cand = p[q] + (uint32_t)wt[q];
-                    key[q] = cand;
-                    if (cand >= (uint32_t)INF) ovf = true;
-                    else if ((int32_t)cand < cur[q]) { old[q] = atomicMin(a.val + v[q], (int32_t)cand); tried[q] = true; }
-                } else if (ALGO == BFS) {
-                    if (cur[q] == INF) {
-                        old[q] = (int32_t)atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
-                        tried[q] = true;
-                    }
-                } else {
-                    const uint32_t lu = p[q], lv = (uint32_t)cur[q];
-                    if (lu != lv) {
-                        const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                        key[q] = lo;
-                        old[q] = atomicMin(a.val + hi, (int32_t)lo);
-                        tried[q] = true;
-                    }
-                }
-            }
             bool need[U];
             uint32_t citem[U];
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 need[q] = false; citem[q] = 0;
-                if (!tried[q]) continue;
+                if (!ok[q]) continue;
                 if (ALGO == SSSP) {
-                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; need[q] = true; citem[q] = v[q]; }
-                } else if (ALGO == BFS) {
-                    if (!((uint32_t)old[q] & (1u << (v[q] & 31)))) {
-                        a.val[v[q]] = (int32_t)(lev + 1);
-                        nu++; chg = true;
-                        if (STYLE == WORKLIST) { need[q] = true; citem[q] = v[q]; }
-                        else atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
+                    const uint32_t cand = p[q] + (uint32_t)wt[q];
+                    if (cand >= (uint32_t)INF) {
+                        ovf = true;
+                    } else if ((int32_t)cand < cur[q]) {
+                        atomicMin(a.val + v[q], (int32_t)cand);   // result unused: RED.MIN
+                        nu++; chg = true; need[q] = true; citem[q] = v[q];
                     }
-                } else {
-                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; }
-                    if (STYLE == WORKLIST) { need[q] = true; citem[q] = uj[q]; }
+                } else if (ALGO == BFS) {
+                    // t.dist > lev+1 -> t.dist = lev+1 (plain store;
+                    // concurrent writers store the same value, R9)
+                    if (cur[q] == INF) {
+                        if (STYLE == WORKLIST) {   // the queue needs exactly-once: claim
+                            need[q] = true; citem[q] = v[q];
+                        } else {   // the level is written by the next round's k_scan
+                            atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
+                            atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
+                            nu++; chg = true;
+                        }
+                    }
+                } else {   // CC: hook the larger root under the smaller (min-label)
+                    const uint32_t lu = p[q], lv = (uint32_t)cur[q];
+                    if (lu != lv) {
+                        const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
+                        atomicMin(a.val + hi, (int32_t)lo);   // RED.MIN
+                        nu++; chg = true;
+                        if (STYLE == WORKLIST) { need[q] = true; citem[q] = uj[q]; }   // keep u while unresolved
+                    }
                 }
             }
-            uint32_t got[U];
+            if (STYLE == VERTEX) {
+                if (ALGO == SSSP) {
 #pragma unroll
-            for (int q = 0; q < U; q++) {
-                got[q] = 0xffffffffu;
-                if (!need[q]) continue;
-                if (ALGO == BFS) { got[q] = 0; continue; }
-                const uint32_t b = 1u << (citem[q] & 31);
-                if (STYLE == WORKLIST) got[q] = atomicOr(bm_now + (citem[q] >> 5), b);
-                else atomicOr(bm_now + (citem[q] >> 5), b);
-            }
-            if (STYLE == WORKLIST) {
+                    for (int q = 0; q < U; q++)
+                        if (need[q]) atomicOr(bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
+                }
+            } else {
+                uint32_t got[U];
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    got[q] = 0xffffffffu;
+                    if (!need[q]) continue;
+                    uint32_t *bmp = ALGO == BFS ? a.vis : bm_now;
+                    got[q] = atomicOr(bmp + (citem[q] >> 5), 1u << (citem[q] & 31));
+                }
 #pragma unroll
                 for (int q = 0; q < U; q++) {
                     const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
+                    if (ALGO == BFS && want) { a.val[citem[q]] = (int32_t)(lev + 1); nu++; chg = true; }
                     const unsigned mask = __ballot_sync(FULL, want);
                     if (want) wq[qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
                     qn += __popc(mask);
@@ -662,14 +783,82 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         }
     }
     if (STYLE == WORKLIST) { __syncwarp(); wflush(0); }
-    flush_counters<B>(a, nv, ne, nu, chg, ovf);
+    flush_counters<B>(a, nv, ne, nu, chg, ovf, ALGO == BFS && STYLE == VERTEX);
 }
 
 // ------------------------------------------------------------------ EDGE style (COO)
-// Four CSR-ordered arcs per thread per step through 16-byte loads of src,
-// col and w; the source's activity bit (bm[(r-1)%3], L1/L2-resident) decides
-// whether col/w are fetched at all.
-template <int ALGO, int B>
+// QP quads of four CSR-ordered arcs per thread per step: all QP 16-byte src
+// loads are issued first and the sources' activity bits (bm[(r-1)%3],
+// L1/L2-resident) tested, so a mostly-inactive round streams src[] with QP
+// loads in flight per thread; col/w are fetched only for quads with an
+// active source.
+template <int ALGO>
+__device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint32_t (&s)[4], uint32_t actmask,
+                                          uint32_t m4, uint32_t tail, uint32_t lev, uint32_t *bm_now, uint64_t pf,
+                                          uint64_t pl, unsigned long long &ne, unsigned long long &nu, bool &chg,
+                                          bool &ovf) {
+    uint32_t d[4] = {0, 0, 0, 0}, pay[4] = {0, 0, 0, 0};
+    int32_t ww[4] = {0, 0, 0, 0};
+    if (q < m4) {
+        if (ALGO == SSSP) {
+            const uint4 x0 = ld_stream4(a.cw + 4ull * q, pf), x1 = ld_stream4(a.cw + 4ull * q + 2, pf);
+            d[0] = x0.x; ww[0] = (int32_t)x0.y; d[1] = x0.z; ww[1] = (int32_t)x0.w;
+            d[2] = x1.x; ww[2] = (int32_t)x1.y; d[3] = x1.z; ww[3] = (int32_t)x1.w;
+        } else {
+            const uint4 d4 = ld_stream4(a.col + 4ull * q, pf);
+            d[0] = d4.x; d[1] = d4.y; d[2] = d4.z; d[3] = d4.w;
+        }
+    } else {
+        for (uint32_t j = 0; j < tail; j++) {
+            if (ALGO == SSSP) {
+                const uint2 x = ld_stream2(a.cw + 4ull * q + j, pf);
+                d[j] = x.x; ww[j] = (int32_t)x.y;
+            } else {
+                d[j] = ld_stream(a.col + 4ull * q + j, pf);
+            }
+        }
+    }
+    int32_t cur[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        cur[j] = 0;
+        if (!((actmask >> j) & 1u)) continue;
+        if (ALGO != BFS) pay[j] = (uint32_t)ld_val(a.val + s[j], pl);   // consecutive arcs share a source
+        if (ALGO == BFS) cur[j] = bit_test(a.vis, d[j]) ? 0 : INF;
+        else cur[j] = ld_val(a.val + d[j], pl);
+    }
+    // fire-and-forget relaxations (reductions), see k_expand_warp
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (!((actmask >> j) & 1u)) continue;
+        ne++;
+        if (ALGO == SSSP) {
+            const uint32_t cand = pay[j] + (uint32_t)ww[j];
+            if (cand >= (uint32_t)INF) { ovf = true; continue; }
+            if ((int32_t)cand < cur[j]) {
+                atomicMin(a.val + d[j], (int32_t)cand);
+                atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
+                nu++; chg = true;
+            }
+        } else if (ALGO == BFS) {   // e.src.dist == lev (R14) via the bitmap
+            if (cur[j] == INF) {
+                atomicOr(a.vis + (d[j] >> 5), 1u << (d[j] & 31));
+                a.val[d[j]] = (int32_t)(lev + 1);
+                atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
+                nu++; chg = true;
+            }
+        } else {
+            const uint32_t lu = pay[j], lv = (uint32_t)cur[j];
+            if (lu != lv) {
+                const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
+                atomicMin(a.val + hi, (int32_t)lo);
+                nu++; chg = true;
+            }
+        }
+    }
+}
+
+template <int ALGO, int B, int QP>
 __global__ void __launch_bounds__(B) k_edge(Args a) {
     Ctrl *c = a.ctrl;
     if (c->done) return;
@@ -682,94 +871,33 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
     const uint32_t nq = m4 + (tail ? 1u : 0u);
     unsigned long long ne = 0, nu = 0;
     bool chg = false, ovf = false;
-    for (uint32_t q = blockIdx.x * B + threadIdx.x; q < nq; q += gridDim.x * B) {
-        const uint32_t cntq = q < m4 ? 4u : tail;
-        uint32_t s[4] = {0, 0, 0, 0}, d[4] = {0, 0, 0, 0}, pay[4] = {0, 0, 0, 0};
-        int32_t ww[4] = {0, 0, 0, 0};
-        if (q < m4) {
-            const uint4 s4 = ld_stream4(a.src + 4ull * q, pf);
-            s[0] = s4.x; s[1] = s4.y; s[2] = s4.z; s[3] = s4.w;
-        } else {
-            for (uint32_t j = 0; j < cntq; j++) s[j] = ld_stream(a.src + 4ull * q + j, pf);
-        }
-        bool act[4];
-        bool any = false;
+    const uint32_t stride = gridDim.x * B;
+    for (uint32_t q0 = blockIdx.x * B + threadIdx.x; q0 < nq; q0 += stride * QP) {
+        uint32_t s[QP][4];
+        uint32_t act[QP];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            // ALGO == CC: every arc hooks; otherwise the source must be active
-            act[j] = (uint32_t)j < cntq && (ALGO == CC || bit_test(bm_prev, s[j]));
-            any |= act[j];
-        }
-        if (!any) continue;
-        if (q < m4) {
-            const uint4 d4 = ld_stream4(a.col + 4ull * q, pf);
-            d[0] = d4.x; d[1] = d4.y; d[2] = d4.z; d[3] = d4.w;
-            if (ALGO == SSSP) {
-                const int4 w4 = ld_stream4(a.w + 4ull * q, pf);
-                ww[0] = w4.x; ww[1] = w4.y; ww[2] = w4.z; ww[3] = w4.w;
-            }
-        } else {
-            for (uint32_t j = 0; j < cntq; j++) {
-                d[j] = ld_stream(a.col + 4ull * q + j, pf);
-                if (ALGO == SSSP) ww[j] = ld_stream(a.w + 4ull * q + j, pf);
-            }
-        }
-        int32_t cur[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            cur[j] = 0;
-            if (!act[j]) continue;
-            if (ALGO != BFS) pay[j] = (uint32_t)ld_val(a.val + s[j], pl);   // consecutive arcs share a source
-            if (ALGO == BFS) cur[j] = bit_test(a.vis, d[j]) ? 0 : INF;
-            else cur[j] = ld_val(a.val + d[j], pl);
-        }
-        // phased like k_expand: all four atomics in flight before any result is used
-        int32_t old[4];
-        uint32_t key[4];
-        bool tried[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            tried[j] = false; old[j] = 0; key[j] = 0;
-            if (!act[j]) continue;
-            ne++;
-            if (ALGO == SSSP) {
-                const uint32_t cand = pay[j] + (uint32_t)ww[j];
-                key[j] = cand;
-                if (cand >= (uint32_t)INF) { ovf = true; continue; }
-                if ((int32_t)cand < cur[j]) { old[j] = atomicMin(a.val + d[j], (int32_t)cand); tried[j] = true; }
-            } else if (ALGO == BFS) {   // e.src.dist == lev (R14) via the bitmap
-                if (cur[j] == INF) {
-                    old[j] = (int32_t)atomicOr(a.vis + (d[j] >> 5), 1u << (d[j] & 31));
-                    tried[j] = true;
-                }
-            } else {
-                const uint32_t lu = pay[j], lv = (uint32_t)cur[j];
-                if (lu != lv) {
-                    const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                    key[j] = lo;
-                    old[j] = atomicMin(a.val + hi, (int32_t)lo);
-                    tried[j] = true;
-                }
+        for (int p = 0; p < QP; p++) {
+            const uint32_t q = q0 + p * stride;
+            s[p][0] = s[p][1] = s[p][2] = s[p][3] = 0;
+            if (q < m4) {
+                const uint4 s4 = ld_stream4(a.src + 4ull * q, pf);
+                s[p][0] = s4.x; s[p][1] = s4.y; s[p][2] = s4.z; s[p][3] = s4.w;
+            } else if (q < nq) {
+                for (uint32_t j = 0; j < tail; j++) s[p][j] = ld_stream(a.src + 4ull * q + j, pf);
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            if (!tried[j]) continue;
-            if (ALGO == SSSP) {
-                if ((int32_t)key[j] < old[j]) {
-                    atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
-                    nu++; chg = true;
-                }
-            } else if (ALGO == BFS) {
-                if (!((uint32_t)old[j] & (1u << (d[j] & 31)))) {
-                    a.val[d[j]] = (int32_t)(lev + 1);
-                    atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
-                    nu++; chg = true;
-                }
-            } else {
-                if ((int32_t)key[j] < old[j]) { nu++; chg = true; }
-            }
+        for (int p = 0; p < QP; p++) {
+            const uint32_t q = q0 + p * stride;
+            const uint32_t cntq = q < m4 ? 4u : (q < nq ? tail : 0u);
+            act[p] = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++)   // ALGO == CC: every arc hooks; otherwise the source must be active
+                if ((uint32_t)j < cntq && (ALGO == CC || bit_test(bm_prev, s[p][j]))) act[p] |= 1u << j;
         }
+#pragma unroll
+        for (int p = 0; p < QP; p++)
+            if (act[p]) edge_quad<ALGO>(a, q0 + p * stride, s[p], act[p], m4, tail, lev, bm_now, pf, pl, ne, nu, chg, ovf);
     }
     flush_counters<B>(a, 0ull, ne, nu, chg, ovf);
 }
@@ -793,8 +921,9 @@ __global__ void k_compress(Args a) {
 // Decides on the device whether another round runs ("if
 // (changed == 0) break" / SPEC.md:221 "worklist non-empty"), and drives the
 // CUDA-graph WHILE node through cudaGraphSetConditional.
-template <int STYLE>
-__global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round) {
+template <int ALGO, int STYLE>
+__global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
+                          uint32_t n, uint32_t pull_div) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (c->done) {
         if (in_graph) cudaGraphSetConditional(h, 0);
@@ -814,7 +943,10 @@ __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, u
             c->all_active = 0;
         } else if (STYLE == VERTEX) {
             c->in_len = 0;   // k_scan rebuilds the frontier of the next round
+            // direction-optimising BFS: bottom-up while the next frontier is large
+            if (ALGO == BFS) c->pull = pull_div && c->found > n / pull_div;
         }
+        c->found = 0;
     } else {
         c->done = 1;
     }
@@ -859,6 +991,54 @@ __global__ void k_validate(uint32_t n, uint32_t m, const uint32_t *row_off, cons
         if (w && w[e] < 0) f |= 4;
     }
     if (f) atomicOr(flags, f);
+}
+
+__global__ void k_interleave(uint64_t m, const uint32_t *col, const int32_t *w, uint2 *cw) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride)
+        cw[e] = make_uint2(col[e], (uint32_t)w[e]);
+}
+
+// Reverse CSR (in-arcs), built on the device: in-degree histogram, scan,
+// scatter (in-row order is arbitrary: BFS levels do not depend on it).
+__global__ void k_indeg(uint64_t m, const uint32_t *col, uint32_t *cnt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) atomicAdd(cnt + col[e], 1u);
+}
+// exclusive scan of x[0..len) in place, tiles of 1024 (two-level, second
+// level over tile sums done by k_scan_tiles with one CTA)
+__global__ void k_scan_local(uint32_t *x, uint64_t len, uint32_t *tile_sums) {
+    __shared__ uint32_t s_warp[32];
+    const uint64_t i0 = (uint64_t)blockIdx.x * 1024 + threadIdx.x * 4;
+    uint32_t v[4], sum = 0;
+    for (int j = 0; j < 4; j++) { v[j] = i0 + j < len ? x[i0 + j] : 0; sum += v[j]; }
+    uint32_t total;
+    uint32_t run = block_excl_scan<256>(sum, total, s_warp);
+    for (int j = 0; j < 4; j++) { if (i0 + j < len) x[i0 + j] = run; run += v[j]; }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+__global__ void k_scan_tiles(uint32_t *tile_sums, uint32_t ntiles) {
+    __shared__ uint32_t s_warp[32];
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < ntiles; b0 += 1024) {
+        const uint32_t i0 = b0 + threadIdx.x * 4;
+        uint32_t v[4], sum = 0;
+        for (int j = 0; j < 4; j++) { v[j] = i0 + j < ntiles ? tile_sums[i0 + j] : 0; sum += v[j]; }
+        uint32_t total;
+        uint32_t run = block_excl_scan<256>(sum, total, s_warp) + carry;
+        for (int j = 0; j < 4; j++) { if (i0 + j < ntiles) tile_sums[i0 + j] = run; run += v[j]; }
+        carry += total;
+    }
+}
+__global__ void k_scan_add(uint32_t *x, uint64_t len, const uint32_t *tile_sums) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < len) x[i] += tile_sums[i / 1024];
+}
+__global__ void k_rev_scatter(uint32_t n, const uint32_t *row_off, const uint32_t *col, uint32_t *cursor,
+                              uint32_t *rin_col) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride)
+        for (uint32_t e = row_off[u]; e < row_off[u + 1]; e++) rin_col[atomicAdd(cursor + col[e], 1u)] = u;
 }
 
 __global__ void k_fill_i32(int32_t *p, uint64_t len, int32_t x) {

@@ -35,7 +35,14 @@ for nm in ("cudaDevAttrMaxPersistingL2CacheSize", "cudaDevAttrMaxAccessPolicyWin
     except Exception as e:
         print(nm, "?", e)
 t = time.time()
-G = gg.config(a.config)
+if a.config.startswith("er:"):   # er:n:m:seed
+    _, n_, m_, sd_ = a.config.split(":")
+    G = gg.er(int(n_), int(m_), int(sd_))
+elif a.config.startswith("rmat:"):
+    _, n_, m_, sd_ = a.config.split(":")
+    G = gg.rmat(int(n_), int(m_), int(sd_))
+else:
+    G = gg.config(a.config)
 print(f"gen {a.config}: n={G.n} m={G.m} {time.time()-t:.1f}s", flush=True)
 g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, stream=torch.cuda.current_stream(),
                       flags=fb.LOAD_BUILD_COO)
