@@ -20,6 +20,7 @@
 
 #include "../../include/falcon.h"
 #include "kernels.cuh"
+#include "cc.cuh"
 
 using namespace fk;
 
@@ -83,7 +84,7 @@ struct falcon_graph {
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_expand_all = 0, grid_expand_fr = 0, grid_scan = 0, grid_pull = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    int grid_expand_all = 0, grid_expand_fr = 0, grid_scan = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
     cudaGraph_t graphs[3][3] = {};
     cudaGraphExec_t execs[3][3] = {};
     bool profiling = false;
@@ -213,7 +214,6 @@ int launch_round(falcon_graph *g, int algo, int style, cudaStream_t s, cudaGraph
     if (algo == A && style == S) return Round<A, S>::launch(g, s, h, in_graph, tr);
     R(SSSP, VERTEX) R(SSSP, EDGE) R(SSSP, WORKLIST)
     R(BFS, VERTEX) R(BFS, EDGE) R(BFS, WORKLIST)
-    R(CC, VERTEX) R(CC, EDGE) R(CC, WORKLIST)
 #undef R
     return 0;
 }
@@ -297,7 +297,7 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
     }
-    if (algo == BFS && style == VERTEX && g->pull_div) {
+    if ((algo == BFS && style == VERTEX && g->pull_div) || (algo == CC && style == WORKLIST)) {
         falcon_status_t st = ensure_reverse(g);
         if (st != FALCON_OK) return st;
     }
@@ -312,7 +312,49 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
 
     double relax_ms = -1.0;
     int64_t relax_launches = 0;
-    if (!g->profiling) {
+    int64_t cc_passes = 0, cc_launches = 0;
+    if (algo == CC) {
+        // Fixed pass sequence (no fixpoint loop): union-find hooking is exact
+        // after one pass over the arcs (cc.cuh).
+        Tracer tr{g};
+        Tracer *t = g->profiling ? &tr : nullptr;
+        auto relax_mark = [&](const char *nm) { if (t) t->mark(s, nm, 0); };
+        auto other_mark = [&](const char *nm) { if (t) t->mark(s, nm, 1); };
+        other_mark("begin");
+        if (style == VERTEX) {
+            launch_l2(g, k_cc_vertex<BLOCK>, g->grid_cc, s, a);
+            relax_mark("cc_vertex");
+            cc_passes = 1;
+        } else if (style == EDGE) {
+            launch_l2(g, k_cc_edge<BLOCK>, g->grid_small, s, a);
+            relax_mark("cc_edge");
+            cc_passes = 1;
+        } else {
+            launch_l2(g, k_cc_sample<2>, g->grid_small, s, a);
+            relax_mark("cc_sample");
+            launch_l2(g, k_compress, g->grid_small, s, a);
+            other_mark("compress");
+            k_cc_giant<<<1, 1024, 0, s>>>(a);
+            other_mark("cc_giant");
+            launch_l2(g, k_cc_rest<BLOCK>, g->grid_cc, s, a);
+            relax_mark("cc_rest");
+            cc_passes = 2;
+            cc_launches += 4;
+        }
+        launch_l2(g, k_compress, g->grid_small, s, a);
+        other_mark("compress");
+        cc_launches += 2;
+        CU(cudaGetLastError());
+        if (t) {
+            relax_ms = 0.0;
+            for (size_t i = 1; i < tr.marks.size(); i++) {
+                float ms = 0.f;
+                CU(cudaEventSynchronize(tr.marks[i].ev));
+                CU(cudaEventElapsedTime(&ms, tr.marks[i - 1].ev, tr.marks[i].ev));
+                if (tr.marks[i].kind == 0) { relax_ms += ms; relax_launches++; }
+            }
+        }
+    } else if (!g->profiling) {
         falcon_status_t st = build_graph(g, algo, style);
         if (st != FALCON_OK) return st;
         CU(cudaGraphLaunch(g->execs[algo][style], s));
@@ -365,11 +407,11 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     if (stats) {
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-        stats->iterations = c.iter;
+        stats->iterations = algo == CC ? cc_passes : c.iter;
         stats->vertices_processed = (int64_t)c.vertices;
         stats->edges_relaxed = (int64_t)c.edges;
         stats->updates = (int64_t)c.updates;
-        stats->kernel_launches = (int64_t)c.launches;
+        stats->kernel_launches = (int64_t)c.launches + cc_launches;
         stats->ms = ms;
         stats->relax_ms = relax_ms;
         stats->relax_launches = relax_launches;
@@ -462,12 +504,13 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP - 1) / (BLOCK * EDGE_QP), full(occ_e));
     g->grid_scan = clampg((g->nwords + 4 * BLOCK - 1) / (4 * BLOCK), (int64_t)g->num_sms * 4);
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
+    g->grid_cc = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_expand_all;
-    if (g->grid_expand_fr > slots) slots = g->grid_expand_fr;
-    if (g->grid_edge > slots) slots = g->grid_edge;
+    for (int gsz : {g->grid_expand_fr, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull, g->grid_scan})
+        if (gsz > slots) slots = gsz;
     g->cnt_slots = slots;
     CU(dmalloc(&g->cnt, 3 * (size_t)slots));
 
