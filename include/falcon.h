@@ -53,7 +53,9 @@ extern "C" {
 typedef enum {
     FALCON_STYLE_VERTEX = 0,   /* topology-driven over CSR rows   */
     FALCON_STYLE_EDGE = 1,     /* topology-driven over COO arcs   */
-    FALCON_STYLE_WORKLIST = 2  /* data-driven over a frontier queue */
+    FALCON_STYLE_WORKLIST = 2, /* data-driven over a frontier queue */
+    FALCON_STYLE_DELTA = 3     /* SSSP only: Δ-stepping bucketed worklist (near queue + far set;
+                                  PAPER.md:454).  Same result. */
 } falcon_style_t;
 
 typedef enum {
@@ -129,6 +131,13 @@ FALCON_API falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon
  * SPEC.md:452).  Weights and arc direction are ignored.
  * label_out: (host|device) int32[n]. */
 FALCON_API falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats);
+
+/* Bucket width Δ of FALCON_STYLE_DELTA (SSSP): vertices with tentative
+ * distance < T are relaxed from the near queue, the others wait in a far set
+ * until the near queue is empty and T advances to the next non-empty bucket.
+ * delta == 0 (default) = max(1, average arc weight).
+ * Errors: INVALID_ARG (g NULL or delta < 0). */
+FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
 
 /* Profiling mode (off by default): when on, the fixpoint loop is driven from
  * the host and every relax-kernel launch is bracketed by CUDA events, filling

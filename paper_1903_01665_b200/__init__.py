@@ -14,12 +14,12 @@ import ctypes
 import os
 
 __all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "falcon_sssp", "falcon_bfs", "falcon_cc",
-           "falcon_set_profiling", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
+           "falcon_set_profiling", "falcon_set_delta", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
 
 INF = 2147483647
-STYLE_VERTEX, STYLE_EDGE, STYLE_WORKLIST = 0, 1, 2
-STYLES = {"vertex": STYLE_VERTEX, "edge": STYLE_EDGE, "worklist": STYLE_WORKLIST}
+STYLE_VERTEX, STYLE_EDGE, STYLE_WORKLIST, STYLE_DELTA = 0, 1, 2, 3
+STYLES = {"vertex": STYLE_VERTEX, "edge": STYLE_EDGE, "worklist": STYLE_WORKLIST, "delta": STYLE_DELTA}
 LOAD_BUILD_COO = 0x1
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "NO_MEMORY", 4: "CUDA", 5: "OVERFLOW",
           6: "NOT_CONVERGED", 7: "COMM", 8: "UNSUPPORTED"}
@@ -70,6 +70,8 @@ def load(build_if_missing: bool = False):
     lib.falcon_bfs.argtypes = [p, u32, ctypes.c_int, p, ctypes.POINTER(FalconStats)]
     lib.falcon_cc.argtypes = [p, ctypes.c_int, p, ctypes.POINTER(FalconStats)]
     lib.falcon_set_profiling.argtypes = [p, ctypes.c_int]
+    lib.falcon_set_delta.argtypes = [p, ctypes.c_int32]
+    lib.falcon_set_delta.restype = st
     for f in (lib.graph_load_csr, lib.graph_free, lib.graph_info, lib.falcon_sssp, lib.falcon_bfs, lib.falcon_cc,
               lib.falcon_set_profiling):
         f.restype = st
@@ -184,6 +186,11 @@ def falcon_cc(g: Graph, style, label_out) -> FalconStats:
 
 def falcon_set_profiling(g: Graph, enable: bool):
     _check(load().falcon_set_profiling(g.handle, int(bool(enable))))
+
+
+def falcon_set_delta(g: Graph, delta: int):
+    """Bucket width of the DELTA style (0 = auto: max(1, average weight))."""
+    _check(load().falcon_set_delta(g.handle, int(delta)))
 
 
 def falcon_last_error() -> str:

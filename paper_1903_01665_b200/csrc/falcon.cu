@@ -27,8 +27,6 @@ using namespace fk;
 namespace {
 
 constexpr int BLOCK = 256;
-constexpr int IPT_ALL = 4;  // items per thread per tile when every vertex is an item (CC VERTEX)
-constexpr int IPT_FR = 1;   // frontier items per thread per tile
 constexpr int UNROLL = 4;   // arcs per thread per expansion step
 constexpr int EDGE_QP = 4;   // 4-arc quads per thread per step (EDGE style)
 constexpr int MINB = 4;     // min resident CTAs per SM for the warp-centric expansion
@@ -84,14 +82,16 @@ struct falcon_graph {
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_expand_all = 0, grid_expand_fr = 0, grid_scan = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
-    cudaGraph_t graphs[3][3] = {};
-    cudaGraphExec_t execs[3][3] = {};
+    int grid_persist = 0, grid_expand_fr = 0, grid_scan = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    cudaGraph_t graphs[3][4] = {};
+    cudaGraphExec_t execs[3][4] = {};
+    int32_t delta = 0;                   // DELTA bucket width (0 = auto: max(1, average weight))
+    int32_t delta_auto = 0;
     bool profiling = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> pev;
     int variant = 0;                     // FALCON_EXPAND_VARIANT
-    bool warp_expand = true;             // warp-centric expansion (FALCON_EXPAND=cta for the CTA-tile kernel)
+    bool persist = true;                 // queue styles run all rounds in one cooperative kernel (FALCON_PERSIST=0: per-round launches)
     bool l2_window = false;              // persisting L2 access-policy window on val[]
     cudaAccessPolicyWindow apw = {};
 
@@ -142,6 +142,29 @@ struct Tracer {
 
 // Expansion-kernel variants (arcs per lane per step U, min resident CTAs per
 // SM): selected at load time by FALCON_EXPAND_VARIANT (tuning experiments).
+// Cooperative launch (all CTAs co-resident: the persistent kernel's grid
+// barrier relies on it), with the same L2 access-policy window.
+template <typename... KArgs, typename... Act>
+cudaError_t launch_coop(const falcon_graph *g, void (*k)(KArgs...), int grid, cudaStream_t s, Act &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(BLOCK);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    na++;
+    if (g->l2_window) {
+        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[na].val.accessPolicyWindow = g->apw;
+        na++;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...);
+}
+
 template <int ALGO, int STYLE>
 void launch_expand_warp(const falcon_graph *g, cudaStream_t s, const Args &a) {
     switch (g->variant) {
@@ -160,11 +183,7 @@ struct Round {
         Args a = g->args();
         int launches = 0;
         if (tr) tr->mark(s, "begin", 1);
-        if (STYLE == VERTEX && ALGO == CC) {
-            if (g->warp_expand) launch_expand_warp<ALGO, VERTEX>(g, s, a);
-            else launch_l2(g, k_expand<ALGO, VERTEX, BLOCK, IPT_ALL, UNROLL>, g->grid_expand_all, s, a);
-            if (tr) tr->mark(s, "expand", 0);
-        } else if (STYLE == VERTEX) {
+        if (STYLE == VERTEX) {
             launch_l2(g, k_scan<ALGO, BLOCK>, g->grid_scan, s, a);
             launches++;
             if (tr) tr->mark(s, "scan", 0);
@@ -173,23 +192,22 @@ struct Round {
                 launches++;
                 if (tr) tr->mark(s, "pull", 0);
             }
-            if (g->warp_expand) launch_expand_warp<ALGO, VERTEX>(g, s, a);
-            else launch_l2(g, k_expand<ALGO, VERTEX, BLOCK, IPT_FR, UNROLL>, g->grid_expand_fr, s, a);
+            launch_expand_warp<ALGO, VERTEX>(g, s, a);
+            if (tr) tr->mark(s, "expand", 0);
+        } else if (STYLE == DELTA) {
+            launch_l2(g, k_scan_far<BLOCK>, g->grid_pull, s, a);
+            launches++;
+            if (tr) tr->mark(s, "scan_far", 0);
+            launch_expand_warp<ALGO, DELTA>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == WORKLIST) {
-            if (g->warp_expand) launch_expand_warp<ALGO, WORKLIST>(g, s, a);
-            else launch_l2(g, k_expand<ALGO, WORKLIST, BLOCK, IPT_FR, UNROLL>, g->grid_expand_fr, s, a);
+            launch_expand_warp<ALGO, WORKLIST>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else {
             launch_l2(g, k_edge<ALGO, BLOCK, EDGE_QP>, g->grid_edge, s, a);
             if (tr) tr->mark(s, "edge", 0);
         }
         launches++;
-        if (ALGO == CC) {
-            launch_l2(g, k_compress, g->grid_small, s, a);
-            launches++;
-            if (tr) tr->mark(s, "compress", 1);
-        }
         launches++;
         k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n, g->pull_div);
         if (tr) tr->mark(s, "advance", 1);
@@ -212,7 +230,7 @@ int launch_round(falcon_graph *g, int algo, int style, cudaStream_t s, cudaGraph
                  Tracer *tr) {
 #define R(A, S) \
     if (algo == A && style == S) return Round<A, S>::launch(g, s, h, in_graph, tr);
-    R(SSSP, VERTEX) R(SSSP, EDGE) R(SSSP, WORKLIST)
+    R(SSSP, VERTEX) R(SSSP, EDGE) R(SSSP, WORKLIST) R(SSSP, DELTA)
     R(BFS, VERTEX) R(BFS, EDGE) R(BFS, WORKLIST)
 #undef R
     return 0;
@@ -290,7 +308,8 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
 falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out, falcon_stats_t *stats) {
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
-    if (style < 0 || style > 2) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
+    if (style < 0 || style > 3) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
+    if (style == DELTA && algo != SSSP) return fail(FALCON_ERR_INVALID_ARG, "FALCON_STYLE_DELTA is an SSSP schedule");
     if (algo != CC && (int64_t)source >= g->n) return fail(FALCON_ERR_INVALID_ARG, "source %u >= n", source);
     CU(cudaSetDevice(g->device));
     if (style == EDGE) {
@@ -304,15 +323,34 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     cudaStream_t s = g->stream;
     Args a = g->args();
     const uint32_t cap = (uint32_t)(g->n + 2 > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : g->n + 2);
+    uint32_t delta = 1;
+    if (style == DELTA) {
+        if (g->delta > 0) {
+            delta = (uint32_t)g->delta;
+        } else {
+            if (!g->delta_auto) {   // average weight, once per graph
+                unsigned long long *d_sum = nullptr, h_sum = 0;
+                CU(dmalloc(&d_sum, 1));
+                CU(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), s));
+                if (g->m) k_sum_weights<<<g->num_sms * 8, BLOCK, 0, s>>>((uint64_t)g->m, g->w, d_sum);
+                CU(cudaMemcpyAsync(&h_sum, d_sum, sizeof h_sum, cudaMemcpyDeviceToHost, s));
+                CU(cudaStreamSynchronize(s));
+                cudaFree(d_sum);
+                const unsigned long long avg = g->m ? h_sum / (unsigned long long)g->m : 1;
+                g->delta_auto = (int32_t)(avg < 1 ? 1 : (avg > 0x3fffffff ? 0x3fffffff : avg));
+            }
+            delta = (uint32_t)g->delta_auto;
+        }
+    }
     CU(cudaEventRecord(g->ev0, s));
-    if (algo == SSSP) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style);
-    else if (algo == BFS) k_init<BFS><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style);
-    else k_init<CC><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style);
+    if (algo == SSSP) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
+    else if (algo == BFS) k_init<BFS><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
+    else k_init<CC><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
     CU(cudaGetLastError());
 
     double relax_ms = -1.0;
     int64_t relax_launches = 0;
-    int64_t cc_passes = 0, cc_launches = 0;
+    int64_t cc_passes = 0, cc_launches = 0, persist_launches = 0;
     if (algo == CC) {
         // Fixed pass sequence (no fixpoint loop): union-find hooking is exact
         // after one pass over the arcs (cc.cuh).
@@ -353,6 +391,24 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
                 CU(cudaEventElapsedTime(&ms, tr.marks[i - 1].ev, tr.marks[i].ev));
                 if (tr.marks[i].kind == 0) { relax_ms += ms; relax_launches++; }
             }
+        }
+    } else if (g->persist && (style == WORKLIST || style == DELTA)) {
+        // all rounds inside one cooperative kernel (k_persist)
+        Tracer tr{g};
+        if (g->profiling) tr.mark(s, "begin", 1);
+        cudaError_t e;
+        if (algo == BFS) e = launch_coop(g, k_persist<BFS, WORKLIST, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div);
+        else if (style == DELTA) e = launch_coop(g, k_persist<SSSP, DELTA, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div);
+        else e = launch_coop(g, k_persist<SSSP, WORKLIST, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div);
+        if (e != cudaSuccess) return fail(FALCON_ERR_CUDA, "cooperative launch of k_persist: %s", cudaGetErrorString(e));
+        persist_launches = 1;
+        if (g->profiling) {
+            tr.mark(s, "persist", 0);
+            float ms = 0.f;
+            CU(cudaEventSynchronize(tr.marks[1].ev));
+            CU(cudaEventElapsedTime(&ms, tr.marks[0].ev, tr.marks[1].ev));
+            relax_ms = ms;
+            relax_launches = 1;
         }
     } else if (!g->profiling) {
         falcon_status_t st = build_graph(g, algo, style);
@@ -411,7 +467,7 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
         stats->vertices_processed = (int64_t)c.vertices;
         stats->edges_relaxed = (int64_t)c.edges;
         stats->updates = (int64_t)c.updates;
-        stats->kernel_launches = (int64_t)c.launches + cc_launches;
+        stats->kernel_launches = (int64_t)c.launches + cc_launches + persist_launches;
         stats->ms = ms;
         stats->relax_ms = relax_ms;
         stats->relax_launches = relax_launches;
@@ -484,23 +540,27 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (m) k_interleave<<<g->num_sms * 8, BLOCK, 0, s>>>((uint64_t)m, g->col, g->w, g->cw);
 
     // grid sizes: a multiple of the SM count x resident CTAs, capped by the work
-    int occ_a = 0, occ_f = 0, occ_e = 0, occ_s = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_expand<CC, VERTEX, BLOCK, IPT_ALL, UNROLL>, BLOCK, 0));
-    const char *ex = getenv("FALCON_EXPAND");
-    g->warp_expand = !(ex && strcmp(ex, "cta") == 0);
+    int occ_f = 0, occ_e = 0, occ_s = 0, occ_p = 0;
     const char *var = getenv("FALCON_EXPAND_VARIANT");
     g->variant = var ? atoi(var) : 0;
     static const int var_minb[5] = {MINB, 8, 2, 3, 6};
-    if (g->warp_expand)
-        occ_f = var_minb[g->variant >= 0 && g->variant < 5 ? g->variant : 0];
-    else
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_expand<SSSP, WORKLIST, BLOCK, IPT_FR, UNROLL>, BLOCK, 0));
+    occ_f = var_minb[g->variant >= 0 && g->variant < 5 ? g->variant : 0];
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_persist<SSSP, DELTA, BLOCK, UNROLL>, BLOCK, 0));
+    {
+        int o2 = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_persist<BFS, WORKLIST, BLOCK, UNROLL>, BLOCK, 0));
+        if (o2 < occ_p) occ_p = o2;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_persist<SSSP, WORKLIST, BLOCK, UNROLL>, BLOCK, 0));
+        if (o2 < occ_p) occ_p = o2;
+    }
+    const char *pe = getenv("FALCON_PERSIST");
+    g->persist = !(pe && pe[0] == '0') && occ_p > 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK, EDGE_QP>, BLOCK, 0));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scan<SSSP, BLOCK>, BLOCK, 0));
     auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };
     auto full = [&](int occ) { return (int64_t)g->num_sms * (occ > 0 ? occ : 1); };
-    g->grid_expand_all = clampg((n + BLOCK * IPT_ALL - 1) / (BLOCK * IPT_ALL), full(occ_a));
-    g->grid_expand_fr = clampg((n + BLOCK * IPT_FR - 1) / (BLOCK * IPT_FR), full(occ_f));
+    g->grid_persist = (int)full(occ_p);
+    g->grid_expand_fr = clampg((n + BLOCK - 1) / BLOCK, full(occ_f));
     g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP - 1) / (BLOCK * EDGE_QP), full(occ_e));
     g->grid_scan = clampg((g->nwords + 4 * BLOCK - 1) / (4 * BLOCK), (int64_t)g->num_sms * 4);
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
@@ -508,7 +568,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
-    int slots = g->grid_expand_all;
+    int slots = g->grid_persist;
     for (int gsz : {g->grid_expand_fr, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull, g->grid_scan})
         if (gsz > slots) slots = gsz;
     g->cnt_slots = slots;
@@ -605,6 +665,13 @@ falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon_style_t st
 
 falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats) {
     return run(g, CC, 0, (int)style, label_out, stats);
+}
+
+falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta) {
+    if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
+    if (delta < 0) return fail(FALCON_ERR_INVALID_ARG, "delta must be >= 0 (0 = auto)");
+    g->delta = delta;
+    return FALCON_OK;
 }
 
 falcon_status_t falcon_set_profiling(falcon_graph_t *g, int enable) {

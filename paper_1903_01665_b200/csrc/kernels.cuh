@@ -32,7 +32,8 @@ constexpr int32_t INF = 0x7fffffff;   // MAX_INT
 constexpr unsigned FULL = 0xffffffffu;
 
 enum Algo : int { SSSP = 0, BFS = 1, CC = 2 };
-enum Style : int { VERTEX = 0, EDGE = 1, WORKLIST = 2 };
+enum Style : int { VERTEX = 0, EDGE = 1, WORKLIST = 2, DELTA = 3 };
+enum DeltaMode : uint32_t { MODE_NEAR = 0, MODE_SCAN = 1 };
 enum DevStatus : int { ST_OK = 0, ST_OVERFLOW = 5, ST_NOT_CONVERGED = 6 };
 
 // Device-resident control block: the convergence decision lives here, so no
@@ -51,6 +52,12 @@ struct Ctrl {
     uint32_t source;
     uint32_t pull;        // BFS VERTEX: this round runs bottom-up (pull over in-arcs)
     uint32_t found;       // BFS: vertices discovered this round (direction heuristic)
+    uint32_t thr;         // DELTA: current bucket threshold T (near: dist < T)
+    uint32_t delta;       // DELTA: bucket width
+    uint32_t minpend;     // DELTA: min tentative distance parked in the far set
+    uint32_t mode;        // DELTA: MODE_NEAR (relax the near queue) / MODE_SCAN (refill from far)
+    uint32_t bar_arrive;  // persistent kernel: CTAs arrived at the grid barrier
+    uint32_t bar_gen;     // persistent kernel: barrier generation
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
     unsigned long long edges;
@@ -201,46 +208,12 @@ __device__ __forceinline__ void clear_next_bitmap(const Args &a, uint32_t r) {
         p[i] = make_uint4(0, 0, 0, 0);
 }
 
-// ------------------------------------------------------------------ block-level frontier queue
-// Appends are staged in shared memory (warp-aggregated shared atomics) and
-// written out with ONE global atomicAdd per flush: a single global counter hit
-// by every warp serialises in one L2 slice.
-template <int B, int QCAP>
-struct BlockQueue {
-    uint32_t *q;      // [QCAP] shared
-    uint32_t *cnt;    // shared
-    uint32_t *base;   // shared
-    __device__ __forceinline__ void push(bool want, uint32_t item) {   // warp-collective
-        const unsigned mask = __ballot_sync(FULL, want);
-        if (mask == 0) return;
-        const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
-        uint32_t b = 0;
-        if (lane == leader) b = atomicAdd(cnt, (uint32_t)__popc(mask));
-        b = __shfl_sync(FULL, b, leader);
-        if (want) q[b + __popc(mask & ((1u << lane) - 1u))] = item;
-    }
-    // block-collective; flushes when more than `thresh` items are staged
-    __device__ __forceinline__ void flush(uint32_t *out, uint32_t *gcounter, uint32_t thresh) {
-        __syncthreads();
-        const uint32_t c = *cnt;
-        if (c > thresh) {
-            if (threadIdx.x == 0) *base = atomicAdd(gcounter, c);
-            __syncthreads();
-            const uint32_t b = *base;
-            for (uint32_t i = threadIdx.x; i < c; i += B) out[b + i] = q[i];
-            __syncthreads();
-            if (threadIdx.x == 0) *cnt = 0;
-            __syncthreads();
-        }
-    }
-};
-
 // ------------------------------------------------------------------ init (fused)
 // SSSP/BFS: dist = MAX_INT, dist[source] = 0;
 // CC: label[v] = v.  Clears the bitmaps (source bit set in bm0 / vis), seeds
 // the frontier and resets the control block, in one launch.
 template <int ALGO>
-__global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, int style) {
+__global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, int style, uint32_t delta) {
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
     for (uint32_t v = t0; v < a.n; v += stride) {
@@ -252,6 +225,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         a.bm0[i] = i == sw ? sb : 0u;
         a.bm1[i] = 0u; a.bm2[i] = 0u;
         if (ALGO == BFS) a.vis[i] = i == sw ? sb : 0u;
+        else if (style == DELTA) a.vis[i] = 0u;   // the far set
     }
     for (uint32_t i = t0; i < cnt_len; i += stride) a.cnt[i] = 0ull;
     if (t0 == 0) {
@@ -263,6 +237,8 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->status = ST_OK; c->source = source;
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
         c->pull = 0; c->found = 0;
+        c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
+        c->bar_arrive = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
 }
@@ -351,6 +327,79 @@ __global__ void __launch_bounds__(B) k_scan(Args a) {
     }
 }
 
+// ------------------------------------------------------------------ DELTA: refill from the far set
+// Δ-stepping (PAPER.md:454 / SPEC.md:415-418, 453-461)
+// as a near/far worklist: the near queue holds vertices below the bucket
+// threshold T, improved vertices at or beyond T are parked in the far set
+// (a bitmap).  When the near queue runs dry, k_advance moves T to the bucket
+// of the smallest parked distance and this kernel moves every parked vertex
+// now below T into the near queue (one warp per 32-vertex word: the far word
+// is rewritten with a plain store), recomputing the minimum of what stays.
+template <bool COHERENT>
+__device__ __forceinline__ void scan_far_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, uint32_t *out,
+                                               unsigned long long &nv) {
+    // lane-per-word (coalesced 128-byte loads of the far bitmap); a lane walks
+    // the set bits of its own word, then the warp compacts its moves
+    uint32_t *bm_now = bm_of(a, iter);
+    const int lane = threadIdx.x & 31;
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+    uint32_t pend_min = 0xffffffffu;
+    for (uint32_t w0 = gt - lane; w0 < a.nwords; w0 += nthreads) {   // warp-uniform
+        const uint32_t wi = w0 + lane;
+        const uint32_t fw = wi < a.nwords ? (COHERENT ? __ldcg(a.vis + wi) : a.vis[wi]) : 0u;
+        uint32_t mv = 0;
+        for (uint32_t x = fw; x; x &= x - 1) {
+            const uint32_t v = wi * 32u + (uint32_t)(__ffs(x) - 1);
+            const uint32_t d = (uint32_t)(COHERENT ? __ldcg(a.val + v) : a.val[v]);
+            if (d < thr) mv |= x & (0u - x);
+            else pend_min = d < pend_min ? d : pend_min;
+        }
+        const uint32_t cnt = __popc(mv);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        if (total == 0) continue;
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&c->out_len, total);
+        b = __shfl_sync(FULL, b, 0) + incl - cnt;
+        if (mv) {
+            a.vis[wi] = fw & ~mv;
+            atomicOr(bm_now + wi, mv);   // these are the near queue of the next round
+            for (uint32_t x = mv; x; x &= x - 1) out[b++] = wi * 32u + (uint32_t)(__ffs(x) - 1);
+        }
+        nv += cnt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(FULL, pend_min, o);
+        pend_min = y < pend_min ? y : pend_min;
+    }
+    if (lane == 0 && pend_min != 0xffffffffu) atomicMin(&c->minpend, pend_min);
+}
+
+template <int B>
+__global__ void __launch_bounds__(B) k_scan_far(Args a) {
+    Ctrl *c = a.ctrl;
+    if (c->done || c->mode != MODE_SCAN) return;
+    unsigned long long nv = 0;
+    scan_far_round<false>(a, c, c->iter, c->thr, c->sel ? a.fr0 : a.fr1, nv);
+    flush_counters<B>(a, nv, 0ull, 0ull, false, false);
+}
+
+// Sum of the arc weights (auto Δ = max(1, average weight)).
+__global__ void k_sum_weights(uint64_t m, const int32_t *w, unsigned long long *sum) {
+    unsigned long long t = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) t += (uint32_t)w[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(sum, t);
+}
+
 // ------------------------------------------------------------------ BFS bottom-up (pull) round
 // Direction-optimising BFS, VERTEX style over `innbrs` (Table
 // "Iterators"): every unvisited vertex scans its in-arcs until it finds a
@@ -390,245 +439,59 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
     flush_counters<B>(a, nv, ne, nu, chg, false, true);
 }
 
-// ------------------------------------------------------------------ expansion (VERTEX / WORKLIST)
-// A CTA takes a tile of B*IPT items (frontier entries, or all vertices for
-// CC), each thread IPT consecutive ones; active items contribute their
-// out-degree, a block scan turns degrees into offsets, and the CTA then walks
-// the tile's concatenated arc ranges B*U arcs at a time, each thread finding
-// its item by binary search in shared memory.  Every arc gets one thread
-// regardless of the degree distribution (cooperative expansion for skewed
-// RMAT degrees), and consecutive threads read consecutive
-// col/w words.
-//   VERTEX  : items = the frontier k_scan compacted (CC: all vertices);
-//             an improvement marks v in bm[r%3] / sets `changed`.
-//   WORKLIST: items = the queue of the previous round; an improvement appends
-//             v once per round (bitmap claim).
-template <int ALGO, int STYLE, int B, int IPT, int U>
-__global__ void __launch_bounds__(B, 4) k_expand(Args a) {
-    static_assert(STYLE == VERTEX || STYLE == WORKLIST, "expand is for VERTEX/WORKLIST");
-    constexpr int TILE = B * IPT;
-    constexpr int QCAP = STYLE == WORKLIST ? 2 * B * U : 1;
-    Ctrl *c = a.ctrl;
-    if (c->done) return;
-    const uint32_t iter = c->iter;
-    const uint32_t lev = iter - 1;   // BFS level being expanded
-    const uint32_t *in = c->sel ? a.fr1 : a.fr0;
-    uint32_t *out = c->sel ? a.fr0 : a.fr1;
-    const bool implicit = ALGO == CC && (STYLE == VERTEX || c->all_active != 0);
-    const uint32_t nitems = implicit ? a.n : c->in_len;
-    uint32_t *bm_now = bm_of(a, iter);
-    if (STYLE == WORKLIST || ALGO == CC) clear_next_bitmap(a, iter);   // VERTEX SSSP/BFS: k_scan clears
-    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
-
-    __shared__ uint32_t s_off[TILE], s_beg[TILE], s_pay[TILE], s_u[TILE];
-    __shared__ uint32_t s_warp[B / 32];
-    __shared__ uint32_t s_q[QCAP];
-    __shared__ uint32_t s_cnt, s_base;
-    if (threadIdx.x == 0) s_cnt = 0;
-    BlockQueue<B, QCAP> bq{s_q, &s_cnt, &s_base};
-    unsigned long long nv = 0, ne = 0, nu = 0;
-    bool chg = false, ovf = false;
-
-    for (uint32_t tb = blockIdx.x * TILE; tb < nitems; tb += gridDim.x * TILE) {
-        uint32_t deg[IPT], beg[IPT], pay[IPT], uu[IPT];
-        uint32_t sum = 0;
-        const uint32_t i0 = tb + threadIdx.x * IPT;
-#pragma unroll
-        for (int j = 0; j < IPT; j++) {
-            const uint32_t idx = i0 + j;
-            deg[j] = 0; beg[j] = 0; pay[j] = 0; uu[j] = 0;
-            if (idx < nitems) {
-                const uint32_t u = implicit ? idx : ld_stream(in + idx, pf);
-                uu[j] = u;
-                bool act = true;
-                uint32_t p = 0;
-                if (ALGO == SSSP) {
-                    p = (uint32_t)ld_val(a.val + u, pl);
-                    act = p != (uint32_t)INF;
-                } else if (ALGO == CC) {
-                    p = (uint32_t)ld_val(a.val + u, pl);   // root label after the previous compress
-                }
-                if (act) {
-                    const uint32_t b0 = ld_ro(a.row_off + u), b1 = ld_ro(a.row_off + u + 1);
-                    beg[j] = b0; deg[j] = b1 - b0; pay[j] = p;
-                    nv++;
-                }
-            }
-            sum += deg[j];
-        }
-        uint32_t total;
-        uint32_t run = block_excl_scan<B>(sum, total, s_warp);
-#pragma unroll
-        for (int j = 0; j < IPT; j++) {
-            const int s = threadIdx.x * IPT + j;
-            s_off[s] = run; s_beg[s] = beg[j]; s_pay[s] = pay[j]; s_u[s] = uu[j];
-            run += deg[j];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) ne += total;
-
-        for (uint32_t base = 0; base < total; base += B * U) {
-            uint32_t e[U], it[U];
-            bool ok[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                const uint32_t k = base + q * B + threadIdx.x;
-                ok[q] = k < total;
-                it[q] = 0; e[q] = 0;
-                if (ok[q]) {   // largest i with s_off[i] <= k
-                    int lo = 0, hi = TILE - 1;
-#pragma unroll
-                    for (int step = 0; step < 16; step++) {
-                        if (lo >= hi) break;
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (s_off[mid] <= k) lo = mid; else hi = mid - 1;
-                    }
-                    it[q] = lo;
-                    e[q] = s_beg[lo] + (k - s_off[lo]);
-                }
-            }
-            uint32_t v[U];
-            int32_t wt[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                v[q] = 0; wt[q] = 0;
-                if (ok[q]) {
-                    if (ALGO == SSSP) {   // one 8-byte (col, w) word: one DRAM burst per row
-                        const uint2 x = ld_stream2(a.cw + e[q], pf);
-                        v[q] = x.x; wt[q] = (int32_t)x.y;
-                    } else {
-                        v[q] = ld_stream(a.col + e[q], pf);
-                    }
-                }
-            }
-            int32_t cur[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                cur[q] = 0;
-                if (ok[q]) {
-                    if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;   // visited filter
-                    else cur[q] = ld_val(a.val + v[q], pl);
-                }
-            }
-            // Phased so that the U arcs' dependent round trips overlap:
-            // (D) the atomics whose old value decides the outcome, (E) the
-            // bitmap claims, (F) the queue pushes.
-            int32_t old[U];
-            uint32_t key[U];   // SSSP: cand; CC: lo; BFS: unused
-            bool tried[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                tried[q] = false; old[q] = 0; key[q] = 0;
-                if (!ok[q]) continue;
-                if (ALGO == SSSP) {
-                    const uint32_t cand = s_pay[it[q]] + (uint32_t)wt[q];
-                    key[q] = cand;
-                    if (cand >= (uint32_t)INF) {
-                        ovf = true;
-                    } else if ((int32_t)cand < cur[q]) {
-                        old[q] = atomicMin(a.val + v[q], (int32_t)cand);
-                        tried[q] = true;
-                    }
-                } else if (ALGO == BFS) {
-                    // t.dist > lev+1 -> t.dist = lev+1; the visited
-                    // claim makes the store (and the append) happen exactly once
-                    if (cur[q] == INF) {
-                        old[q] = (int32_t)atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
-                        tried[q] = true;
-                    }
-                } else {   // CC: hook the larger root under the smaller (min-label)
-                    const uint32_t lu = s_pay[it[q]], lv = (uint32_t)cur[q];
-                    if (lu != lv) {
-                        const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                        key[q] = lo;
-                        old[q] = atomicMin(a.val + hi, (int32_t)lo);
-                        tried[q] = true;
-                    }
-                }
-            }
-            bool need[U];
-            uint32_t citem[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                need[q] = false; citem[q] = 0;
-                if (!tried[q]) continue;
-                if (ALGO == SSSP) {
-                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; need[q] = true; citem[q] = v[q]; }
-                } else if (ALGO == BFS) {
-                    if (!((uint32_t)old[q] & (1u << (v[q] & 31)))) {
-                        a.val[v[q]] = (int32_t)(lev + 1);
-                        nu++; chg = true;
-                        if (STYLE == WORKLIST) { need[q] = true; citem[q] = v[q]; }
-                        else atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
-                    }
-                } else {
-                    if ((int32_t)key[q] < old[q]) { nu++; chg = true; }
-                    if (STYLE == WORKLIST) { need[q] = true; citem[q] = s_u[it[q]]; }   // keep u while unresolved
-                }
-            }
-            uint32_t got[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                got[q] = 0xffffffffu;
-                if (!need[q]) continue;
-                if (ALGO == BFS) { got[q] = 0; continue; }   // the visited claim was the dedup
-                const uint32_t b = 1u << (citem[q] & 31);
-                if (STYLE == WORKLIST) got[q] = atomicOr(bm_now + (citem[q] >> 5), b);
-                else atomicOr(bm_now + (citem[q] >> 5), b);   // no return value: a reduction
-            }
-            if (STYLE == WORKLIST) {
-#pragma unroll
-                for (int q = 0; q < U; q++)
-                    bq.push(need[q] && !(got[q] & (1u << (citem[q] & 31))), citem[q]);
-            }
-            if (STYLE == WORKLIST) bq.flush(out, &c->out_len, QCAP > B * U ? QCAP - B * U : 0);
-        }
-        __syncthreads();
-    }
-    if (STYLE == WORKLIST) bq.flush(out, &c->out_len, 0);
-    flush_counters<B>(a, nv, ne, nu, chg, ovf);
-}
-
 // ------------------------------------------------------------------ warp-centric expansion
-// Same work as k_expand, but a WARP owns 32 items: a shuffle scan turns their
-// degrees into offsets and the warp walks the concatenated arc ranges 32*U
-// arcs at a time, each lane finding its item by a 5-step shuffle binary
-// search.  No block barrier in the loop, so warps drift freely.  The path is
-// bound by the latency of dependent memory round trips, so:
-//  * item loads are software-pipelined two tiles ahead (frontier entry two
-//    tiles ahead, value / row offsets one tile ahead);
+// A WARP owns 32 frontier items (or 32 consecutive vertices): a shuffle scan
+// turns their out-degrees into offsets and the warp walks the concatenated
+// arc ranges 32*U arcs at a time, each lane finding its item by a 5-step
+// shuffle binary search -- every arc gets one lane whatever the degree
+// distribution (cooperative expansion for skewed RMAT degrees, PAPER.md:
+// 441-446) and consecutive lanes read consecutive col/w words.  There is no
+// block barrier in the loop.  The path is bound by dependent random memory
+// round trips (tools/l2probe.cu), so:
+//  * item loads are software-pipelined two tiles ahead;
 //  * VERTEX relaxations are fire-and-forget: the read filter `cand < val[v]`
 //    decides, atomicMin / the bitmap OR are issued as reductions (RED) whose
 //    results nobody waits for.  A vertex whose read passed the filter is
 //    improved in this round -- by us, or by whoever lowered it further after
 //    our read, who marks it too -- so the marked set is exactly the set of
 //    vertices improved this round (R8);
-//  * WORKLIST needs the old bitmap word to append each vertex once.
-template <int ALGO, int STYLE, int B, int U, int MINB>
-__global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
-    static_assert(STYLE == VERTEX || STYLE == WORKLIST, "expand is for VERTEX/WORKLIST");
-    constexpr int NW = B / 32;
-    constexpr int WQ = STYLE == WORKLIST ? 512 : 1;
-    Ctrl *c = a.ctrl;
-    if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull)) return;
-    const uint32_t iter = c->iter;
-    const uint32_t lev = iter - 1;
-    const uint32_t *in = c->sel ? a.fr1 : a.fr0;
-    uint32_t *out = c->sel ? a.fr0 : a.fr1;
-    const bool implicit = ALGO == CC && (STYLE == VERTEX || c->all_active != 0);
-    const uint32_t nitems = implicit ? a.n : c->in_len;
-    uint32_t *bm_now = bm_of(a, iter);
-    if (STYLE == WORKLIST || ALGO == CC) clear_next_bitmap(a, iter);
-    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
-
-    __shared__ uint32_t s_q[NW][WQ];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t *wq = s_q[wid];
-    uint32_t qn = 0;   // warp-uniform count of staged appends
+//  * queue styles (WORKLIST, DELTA) need the old bitmap word to append each
+//    vertex once; the bitmap bits of the items being expanded are cleared on
+//    the way (every set bit of bm[(r-1)%3] is an item of round r), so the
+//    bitmap is clean again when it is reused two rounds later.
+struct RoundAcc {
     unsigned long long nv = 0, ne = 0, nu = 0;
     bool chg = false, ovf = false;
-    const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
+};
+
+// COHERENT: loads of data written earlier in the same (persistent) kernel
+// bypass L1 (ld.global.cg); otherwise the read-only / evict-first paths.
+template <bool COHERENT>
+__device__ __forceinline__ uint32_t ld_item(const uint32_t *p, uint64_t pf) {
+    if (COHERENT) return __ldcg(p);
+    return ld_stream(p, pf);
+}
+template <bool COHERENT>
+__device__ __forceinline__ int32_t ld_value(const int32_t *p, uint64_t pl) {
+    if (COHERENT) return __ldcg(p);
+    return ld_val(p, pl);
+}
+
+template <int ALGO, int STYLE, int U, bool COHERENT>
+__device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, const uint32_t *in,
+                                             uint32_t *out, uint32_t nitems, bool implicit, uint32_t *wq,
+                                             RoundAcc &acc) {
+    constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
+    constexpr int WQ = QUEUE ? 512 : 1;
+    const uint32_t lev = iter - 1;
+    uint32_t *bm_now = bm_of(a, iter);
+    uint32_t *bm_prev = bm_of(a, iter - 1);
+    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t wstride = nwarps * 32;
+    uint32_t qn = 0;   // warp-uniform count of staged appends
+    uint32_t pend_min = 0xffffffffu;
 
     auto wflush = [&](uint32_t thresh) {
         if (qn > thresh) {
@@ -642,7 +505,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         }
     };
     auto item_of = [&](uint32_t idx) -> uint32_t {
-        return idx < nitems ? (implicit ? idx : ld_stream(in + idx, pf)) : 0xffffffffu;
+        return idx < nitems ? (implicit ? idx : ld_item<COHERENT>(in + idx, pf)) : 0xffffffffu;
     };
     // software pipeline: u1 = item of the current tile, u2 = item of the next
     // tile; pay1/beg1/end1 = value and row offsets of the current tile's item
@@ -650,24 +513,24 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     uint32_t u1 = item_of(wb + lane), u2 = item_of(wb + wstride + lane);
     uint32_t pay1 = 0, beg1 = 0, end1 = 0;
     if (u1 != 0xffffffffu) {
-        if (ALGO != BFS) pay1 = (uint32_t)ld_val(a.val + u1, pl);
+        if (ALGO != BFS) pay1 = (uint32_t)ld_value<COHERENT>(a.val + u1, pl);
         beg1 = ld_ro(a.row_off + u1); end1 = ld_ro(a.row_off + u1 + 1);
     }
 
     for (; wb < nitems; wb += wstride) {   // warp-uniform
         const uint32_t u = u1, pay = pay1;
         uint32_t beg = beg1, deg = end1 - beg1;
-        // issue the pipeline's next loads before touching this tile's arcs
         u1 = u2;
         u2 = item_of(wb + 2 * wstride + lane);
         if (u1 != 0xffffffffu) {
-            if (ALGO != BFS) pay1 = (uint32_t)ld_val(a.val + u1, pl);
+            if (ALGO != BFS) pay1 = (uint32_t)ld_value<COHERENT>(a.val + u1, pl);
             beg1 = ld_ro(a.row_off + u1); end1 = ld_ro(a.row_off + u1 + 1);
         } else {
             pay1 = 0; beg1 = 0; end1 = 0;
         }
+        if (QUEUE && ALGO != BFS && u != 0xffffffffu) bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
         if (u == 0xffffffffu || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-        else nv++;
+        else acc.nv++;
 
         uint32_t incl = deg;
 #pragma unroll
@@ -677,7 +540,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         }
         const uint32_t total = __shfl_sync(FULL, incl, 31);
         const uint32_t excl = incl - deg;
-        if (lane == 0) ne += total;
+        if (lane == 0) acc.ne += total;
 
         for (uint32_t base = 0; base < total; base += 32 * U) {
             uint32_t e[U], v[U], p[U], uj[U];
@@ -715,7 +578,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
                 cur[q] = 0;
                 if (ok[q]) {
                     if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;
-                    else cur[q] = ld_val(a.val + v[q], pl);
+                    else cur[q] = ld_value<COHERENT>(a.val + v[q], pl);
                 }
             }
             bool need[U];
@@ -727,30 +590,28 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
                 if (ALGO == SSSP) {
                     const uint32_t cand = p[q] + (uint32_t)wt[q];
                     if (cand >= (uint32_t)INF) {
-                        ovf = true;
+                        acc.ovf = true;
                     } else if ((int32_t)cand < cur[q]) {
                         atomicMin(a.val + v[q], (int32_t)cand);   // result unused: RED.MIN
-                        nu++; chg = true; need[q] = true; citem[q] = v[q];
+                        acc.nu++; acc.chg = true;
+                        if (STYLE == DELTA && cand >= thr) {   // beyond the bucket: park in the far set
+                            atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
+                            pend_min = cand < pend_min ? cand : pend_min;
+                        } else {
+                            need[q] = true; citem[q] = v[q];
+                        }
                     }
                 } else if (ALGO == BFS) {
                     // t.dist > lev+1 -> t.dist = lev+1 (plain store;
                     // concurrent writers store the same value, R9)
                     if (cur[q] == INF) {
-                        if (STYLE == WORKLIST) {   // the queue needs exactly-once: claim
+                        if (QUEUE) {   // the queue needs exactly-once: claim
                             need[q] = true; citem[q] = v[q];
                         } else {   // the level is written by the next round's k_scan
                             atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
                             atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
-                            nu++; chg = true;
+                            acc.nu++; acc.chg = true;
                         }
-                    }
-                } else {   // CC: hook the larger root under the smaller (min-label)
-                    const uint32_t lu = p[q], lv = (uint32_t)cur[q];
-                    if (lu != lv) {
-                        const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                        atomicMin(a.val + hi, (int32_t)lo);   // RED.MIN
-                        nu++; chg = true;
-                        if (STYLE == WORKLIST) { need[q] = true; citem[q] = uj[q]; }   // keep u while unresolved
                     }
                 }
             }
@@ -772,7 +633,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
 #pragma unroll
                 for (int q = 0; q < U; q++) {
                     const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
-                    if (ALGO == BFS && want) { a.val[citem[q]] = (int32_t)(lev + 1); nu++; chg = true; }
+                    if (ALGO == BFS && want) { a.val[citem[q]] = (int32_t)(lev + 1); acc.nu++; acc.chg = true; }
                     const unsigned mask = __ballot_sync(FULL, want);
                     if (want) wq[qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
                     qn += __popc(mask);
@@ -782,8 +643,33 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
             }
         }
     }
-    if (STYLE == WORKLIST) { __syncwarp(); wflush(0); }
-    flush_counters<B>(a, nv, ne, nu, chg, ovf, ALGO == BFS && STYLE == VERTEX);
+    if (QUEUE) { __syncwarp(); wflush(0); }
+    if (STYLE == DELTA) {   // warp-min, one atomicMin per warp
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint32_t y = __shfl_xor_sync(FULL, pend_min, o);
+            pend_min = y < pend_min ? y : pend_min;
+        }
+        if (lane == 0 && pend_min != 0xffffffffu) atomicMin(&c->minpend, pend_min);
+    }
+    if (acc.ovf) c->status = ST_OVERFLOW;
+}
+
+// One round per launch (VERTEX, and the queue styles when not persistent).
+template <int ALGO, int STYLE, int B, int U, int MINB>
+__global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
+    static_assert(STYLE == VERTEX || STYLE == WORKLIST || STYLE == DELTA, "expand is for VERTEX/WORKLIST/DELTA");
+    constexpr int WQ = (STYLE == WORKLIST || STYLE == DELTA) ? 512 : 1;
+    Ctrl *c = a.ctrl;
+    if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull) || (STYLE == DELTA && c->mode != MODE_NEAR)) return;
+    const uint32_t iter = c->iter;
+    const uint32_t thr = STYLE == DELTA ? c->thr : 0xffffffffu;
+    const uint32_t *in = c->sel ? a.fr1 : a.fr0;
+    uint32_t *out = c->sel ? a.fr0 : a.fr1;
+    __shared__ uint32_t s_q[B / 32][WQ];
+    RoundAcc acc;
+    expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, c->in_len, false, s_q[threadIdx.x >> 5], acc);
+    flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf, ALGO == BFS && STYLE == VERTEX);
 }
 
 // ------------------------------------------------------------------ EDGE style (COO)
@@ -922,21 +808,32 @@ __global__ void k_compress(Args a) {
 // (changed == 0) break" / SPEC.md:221 "worklist non-empty"), and drives the
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
-__global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
-                          uint32_t n, uint32_t pull_div) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (c->done) {
-        if (in_graph) cudaGraphSetConditional(h, 0);
-        return;
-    }
+__device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t pull_div) {
+    if (c->done) return false;
     c->launches += launches_per_round;
     bool more = STYLE == WORKLIST ? c->out_len > 0 : c->changed != 0;
+    if (STYLE == DELTA) {
+        if (c->mode == MODE_SCAN) {
+            more = true;                 // the refilled near queue (possibly empty) comes next
+            c->mode = MODE_NEAR;
+        } else if (c->out_len == 0) {    // bucket exhausted: move T to the next non-empty bucket
+            more = c->minpend != 0xffffffffu;
+            if (more) {
+                const uint64_t t = ((uint64_t)c->minpend / c->delta + 1) * c->delta;
+                c->thr = t > 0x7fffffffull ? 0x7fffffffu : (uint32_t)t;
+                c->minpend = 0xffffffffu;   // recomputed by the far scan and later parkings
+                c->mode = MODE_SCAN;
+            }
+        } else {
+            more = true;
+        }
+    }
     if (c->status != ST_OK) more = false;
     if (more && c->iter >= c->cap) { c->status = ST_NOT_CONVERGED; more = false; }
     if (more) {
         c->iter++;
         c->changed = 0;
-        if (STYLE == WORKLIST) {
+        if (STYLE == WORKLIST || (STYLE == DELTA && c->mode == MODE_NEAR)) {
             c->in_len = c->out_len;
             c->out_len = 0;
             c->sel ^= 1u;
@@ -950,7 +847,70 @@ __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, u
     } else {
         c->done = 1;
     }
+    return more;
+}
+
+// Decides on the device whether another round runs ("if
+// (changed == 0) break" / SPEC.md:221 "worklist non-empty"), and drives the
+// CUDA-graph WHILE node through cudaGraphSetConditional.
+template <int ALGO, int STYLE>
+__global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
+                          uint32_t n, uint32_t pull_div) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div);
     if (in_graph) cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// ------------------------------------------------------------------ persistent rounds
+// Queue styles (WORKLIST, DELTA) run ALL their rounds inside one cooperative
+// kernel: a round's expansion, then a grid barrier whose last arriving CTA
+// performs the advance (the same advance_step as k_advance) and releases the
+// others.  A round then costs one barrier (~µs) instead of two kernel launches
+// -- it is what makes the thousands of small rounds of road-like graphs
+// and Δ-stepping buckets affordable.  Data written earlier
+// in the kernel is read with L1-bypassing loads (COHERENT).
+__device__ __forceinline__ uint32_t ldv(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
+
+template <int ALGO, int STYLE>
+__device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32_t pull_div) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t gen = ldv(&c->bar_gen);
+        __threadfence();
+        const uint32_t arrived = atomicAdd(&c->bar_arrive, 1u);
+        if (arrived == gridDim.x - 1) {
+            c->bar_arrive = 0;
+            advance_step<ALGO, STYLE>(c, 0u, n, pull_div);
+            __threadfence();
+            atomicExch(&c->bar_gen, gen + 1u);
+        } else {
+            while (ldv(&c->bar_gen) == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int ALGO, int STYLE, int B, int U>
+__global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div) {
+    static_assert(STYLE == WORKLIST || STYLE == DELTA, "persistent rounds are for the queue styles");
+    __shared__ uint32_t s_q[B / 32][512];
+    Ctrl *c = a.ctrl;
+    RoundAcc acc;
+    for (;;) {
+        if (ldv(&c->done)) break;   // uniform: every CTA reads after the same barrier
+        const uint32_t iter = ldv(&c->iter), sel = ldv(&c->sel);
+        const uint32_t thr = STYLE == DELTA ? ldv(&c->thr) : 0xffffffffu;
+        const uint32_t *in = sel ? a.fr1 : a.fr0;
+        uint32_t *out = sel ? a.fr0 : a.fr1;
+        if (STYLE == DELTA && ldv(&c->mode) == MODE_SCAN)
+            scan_far_round<true>(a, c, iter, thr, out, acc.nv);
+        else
+            expand_round<ALGO, STYLE, U, true>(a, c, iter, thr, in, out, ldv(&c->in_len), false,
+                                               s_q[threadIdx.x >> 5], acc);
+        grid_barrier_advance<ALGO, STYLE>(c, a.n, pull_div);
+    }
+    flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
 }
 
 // Sum the per-CTA counters into the control block.

@@ -23,6 +23,7 @@ ap.add_argument("--style", default="worklist")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--check", action="store_true", help="compare with the oracle (test infrastructure)")
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--delta", type=int, default=0)
 a = ap.parse_args()
 
 try:
@@ -48,6 +49,8 @@ g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, stream=torch.cu
                       flags=fb.LOAD_BUILD_COO)
 if a.profile:
     fb.falcon_set_profiling(g, True)
+if a.delta:
+    fb.falcon_set_delta(g, a.delta)
 out = torch.empty(G.n, dtype=torch.int32, device="cuda")
 algos = a.algo.split(",")
 styles = a.style.split(",")
