@@ -71,6 +71,7 @@ typedef enum {
 } falcon_status_t;
 
 typedef struct falcon_graph falcon_graph_t; /* opaque; owns its device memory */
+typedef struct falcon_comm falcon_comm_t;   /* opaque; multi-GPU communicator (NULL = single GPU) */
 
 /* graph_load_csr options (pass NULL for defaults). */
 #define FALCON_LOAD_BUILD_COO 0x1u  /* build the COO src[] array now (else lazily on first EDGE call) */
@@ -79,6 +80,7 @@ typedef struct {
     int device;          /* CUDA device ordinal; -1 = current device                 */
     void *cuda_stream;   /* cudaStream_t to issue work on; NULL = a stream owned by the graph */
     uint32_t flags;      /* FALCON_LOAD_* bits                                       */
+    falcon_comm_t *comm; /* NULL = single GPU; else a 1-D vertex-partitioned graph    */
 } falcon_load_opts_t;
 
 /* Per-call statistics (all counters are device-side totals for the call). */
@@ -106,6 +108,40 @@ typedef struct {
  * Errors: INVALID_ARG, OUT_OF_RANGE (validated on the device), NO_MEMORY, CUDA. */
 FALCON_API falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col,
                                const int32_t *w, const falcon_load_opts_t *opts, falcon_graph_t **out);
+
+/* ---- multi-GPU: 1-D vertex partition ----
+ * Vertices are split into contiguous ranges of ~m/P arcs each; part q stores
+ * the CSR rows of its range and exchanges boundary values once per round
+ * (grouped ncclReduce(MIN) to the owners, ncclAllReduce(SUM) termination).
+ * Every rank passes the FULL CSR to graph_load_csr (it keeps only its rows)
+ * and calls the algorithms collectively, in the same order; every rank
+ * receives the FULL n-length output.  Results equal the single-GPU ones.
+ * BFS runs as unit-weight SSSP; CC hooks on a replicated label array.  The
+ * processing style is ignored (every part runs the VERTEX round). */
+
+/* Partition boundaries: bounds[q] .. bounds[q+1] is part q's vertex range,
+ * chosen so each part owns ~m/nparts arcs (binary search on row_off).
+ * row_off: HOST uint32[n+1].  bounds: HOST int64[nparts+1].  No GPU needed. */
+FALCON_API falcon_status_t falcon_partition(int64_t n, const uint32_t *row_off, int nparts, int64_t *bounds);
+
+/* 128-byte NCCL unique id for falcon_comm_init (call on one rank, broadcast
+ * it out of band, e.g. with torch.distributed).  Errors: COMM (no NCCL). */
+FALCON_API falcon_status_t falcon_comm_unique_id(void *id128);
+
+/* One rank of an nranks-wide communicator on `device` (one process per GPU;
+ * NCCL over NVLink / NVSwitch).  Errors: INVALID_ARG, COMM, CUDA. */
+FALCON_API falcon_status_t falcon_comm_init(int nranks, int rank, const void *id128, int device, falcon_comm_t **out);
+
+/* A simulated communicator: nparts partitions on the current device of ONE
+ * process, exchanged by device kernels (same partition, relax, apply and
+ * termination code; used to test the partitioned algorithm on one GPU). */
+FALCON_API falcon_status_t falcon_comm_init_simulated(int nparts, falcon_comm_t **out);
+
+FALCON_API falcon_status_t falcon_comm_free(falcon_comm_t *comm);
+
+/* Vertex range [lo, hi) owned by this rank ([0, n) for a single-GPU or a
+ * simulated graph). */
+FALCON_API falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi);
 
 /* Release all device memory of the graph.  NULL is a no-op. */
 FALCON_API falcon_status_t graph_free(falcon_graph_t *g);

@@ -5,8 +5,10 @@ sm_100a kernels.  There is no CPU fallback -- if libfalcon.so cannot be loaded
 every call raises.  Arrays may be numpy arrays (host) or torch tensors (host
 or CUDA); PyTorch is used only for device memory and streams.
 
-Names follow the C ABI: graph_load_csr, graph_free, graph_info, falcon_sssp,
-falcon_bfs, falcon_cc, falcon_set_profiling, falcon_last_error, falcon_version.
+Names follow the C ABI: graph_load_csr, graph_free, graph_info, graph_owned_range,
+falcon_sssp, falcon_bfs, falcon_cc, falcon_set_profiling, falcon_set_delta,
+falcon_partition, falcon_comm_unique_id, falcon_comm_init,
+falcon_comm_init_simulated, falcon_comm_free, falcon_last_error, falcon_version.
 """
 from __future__ import annotations
 
@@ -14,7 +16,8 @@ import ctypes
 import os
 
 __all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "falcon_sssp", "falcon_bfs", "falcon_cc",
-           "falcon_set_profiling", "falcon_set_delta", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
+           "falcon_set_profiling", "falcon_set_delta", "falcon_partition", "falcon_comm_unique_id",
+           "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_free", "graph_owned_range", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
 
 INF = 2147483647
@@ -47,7 +50,8 @@ class FalconStats(ctypes.Structure):
 
 
 class _LoadOpts(ctypes.Structure):
-    _fields_ = [("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint32)]
+    _fields_ = [("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint32),
+                ("comm", ctypes.c_void_p)]
 
 
 def load(build_if_missing: bool = False):
@@ -72,6 +76,15 @@ def load(build_if_missing: bool = False):
     lib.falcon_set_profiling.argtypes = [p, ctypes.c_int]
     lib.falcon_set_delta.argtypes = [p, ctypes.c_int32]
     lib.falcon_set_delta.restype = st
+    lib.falcon_partition.argtypes = [i64, p, ctypes.c_int, p]
+    lib.falcon_comm_unique_id.argtypes = [p]
+    lib.falcon_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, p, ctypes.c_int, ctypes.POINTER(p)]
+    lib.falcon_comm_init_simulated.argtypes = [ctypes.c_int, ctypes.POINTER(p)]
+    lib.falcon_comm_free.argtypes = [p]
+    lib.graph_owned_range.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    for f in (lib.falcon_partition, lib.falcon_comm_unique_id, lib.falcon_comm_init, lib.falcon_comm_init_simulated,
+              lib.falcon_comm_free, lib.graph_owned_range):
+        f.restype = st
     for f in (lib.graph_load_csr, lib.graph_free, lib.graph_info, lib.falcon_sssp, lib.falcon_bfs, lib.falcon_cc,
               lib.falcon_set_profiling):
         f.restype = st
@@ -137,7 +150,63 @@ class Graph:
         return self.handle
 
 
-def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, stream=None, flags: int = 0) -> Graph:
+class Comm:
+    """Owning handle of a falcon_comm_t (multi-GPU or simulated partitions)."""
+
+    def __init__(self, handle: ctypes.c_void_p, nparts: int, rank: int):
+        self.handle = handle
+        self.nparts = nparts
+        self.rank = rank
+
+    def __del__(self):
+        try:
+            falcon_comm_free(self)
+        except Exception:
+            pass
+
+
+def falcon_partition(row_off, nparts: int):
+    """Edge-balanced contiguous vertex ranges: int64[nparts+1] (host only)."""
+    import numpy as np
+    row_off = np.ascontiguousarray(row_off, np.uint32)
+    bounds = np.empty(nparts + 1, np.int64)
+    _check(load().falcon_partition(len(row_off) - 1, _ptr(row_off), nparts, _ptr(bounds)))
+    return bounds
+
+
+def falcon_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().falcon_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def falcon_comm_init(nranks: int, rank: int, unique_id: bytes, device: int) -> Comm:
+    out = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(load().falcon_comm_init(nranks, rank, ctypes.cast(buf, ctypes.c_void_p), device, ctypes.byref(out)))
+    return Comm(out, nranks, rank)
+
+
+def falcon_comm_init_simulated(nparts: int) -> Comm:
+    out = ctypes.c_void_p()
+    _check(load().falcon_comm_init_simulated(nparts, ctypes.byref(out)))
+    return Comm(out, nparts, 0)
+
+
+def falcon_comm_free(comm: Comm):
+    if comm is not None and comm.handle:
+        load().falcon_comm_free(comm.handle)
+        comm.handle = None
+
+
+def graph_owned_range(g: "Graph"):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().graph_owned_range(g.handle, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, stream=None, flags: int = 0,
+                   comm: Comm | None = None) -> Graph:
     """graph_load_csr(n, m, row_off u32[n+1], col u32[m], w i32[m] | None, ...)."""
     lib = load()
     _check_dtype(row_off, "u32", "row_off"); _check_dtype(col, "u32", "col")
@@ -145,10 +214,13 @@ def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, strea
         _check_dtype(w, "i32", "w")
     if stream is not None and hasattr(stream, "cuda_stream"):
         stream = stream.cuda_stream
-    opts = _LoadOpts(device, ctypes.c_void_p(stream) if stream else None, flags)
+    opts = _LoadOpts(device, ctypes.c_void_p(stream) if stream else None, flags,
+                     comm.handle if comm is not None else None)
     out = ctypes.c_void_p()
     _check(lib.graph_load_csr(n, m, _ptr(row_off), _ptr(col), _ptr(w), ctypes.byref(opts), ctypes.byref(out)))
-    return Graph(out, n, m)
+    g = Graph(out, n, m)
+    g._comm = comm   # keep the communicator alive as long as the graph
+    return g
 
 
 def graph_free(g: Graph):

@@ -55,6 +55,7 @@ __device__ __forceinline__ bool uf_unite(int32_t *L, uint32_t a, uint32_t b) {
 // scan / binary search as k_expand_warp), unite(u, v) per arc.
 template <int B>
 __global__ void __launch_bounds__(B) k_cc_vertex(Args a) {
+    if (a.ctrl->done) return;
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
     const uint64_t pf = pol_evict_first();
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(B) k_cc_vertex(Args a) {
             }
         }
     }
-    flush_counters<B>(a, nv, ne, nu, false, false);
+    flush_counters<B>(a, nv, ne, nu, nu != 0, false);   // `changed` = some hook (partitioned rounds)
 }
 
 // EDGE: one arc per thread per step over the COO arrays (coalesced src/col

@@ -95,10 +95,19 @@ struct falcon_graph {
     bool l2_window = false;              // persisting L2 access-policy window on val[]
     cudaAccessPolicyWindow apw = {};
 
+    // ---- 1-D vertex partition (multi-GPU) ----
+    falcon_comm *comm = nullptr;          // non-NULL: this handle is a partitioned graph
+    std::vector<falcon_graph *> parts;    // NCCL: this rank's part; simulated: every part
+    std::vector<int64_t> bounds;          // part q owns vertices [bounds[q], bounds[q+1])
+    int64_t lo = 0, hi = 0;               // (part) owned vertex range
+    int32_t *recv = nullptr;              // (part) owned-range receive buffer of the exchange
+    uint2 *cw_unit = nullptr;             // (part) unit-weight (col, 1) arcs: BFS as unit-weight SSSP
+    bool use_unit = false;
+
     Args args() const {
         Args a;
         a.n = (uint32_t)n; a.m = (uint32_t)m; a.nwords = nwords;
-        a.row_off = row_off; a.col = col; a.w = w; a.cw = cw; a.src = src;
+        a.row_off = row_off; a.col = col; a.w = w; a.cw = use_unit ? cw_unit : cw; a.src = src;
         a.rin_off = rin_off; a.rin_col = rin_col;
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
@@ -305,7 +314,14 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
     return FALCON_OK;
 }
 
+falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int32_t *out, falcon_stats_t *stats);
+
 falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out, falcon_stats_t *stats) {
+    if (g && g->comm) {
+        if (style < 0 || style > 3) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
+        if (style == DELTA && algo != SSSP) return fail(FALCON_ERR_INVALID_ARG, "FALCON_STYLE_DELTA is an SSSP schedule");
+        return run_partitioned(g, algo, source, out, stats);
+    }
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
     if (style < 0 || style > 3) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
@@ -478,8 +494,15 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     return FALCON_OK;
 }
 
+void destroy_partitioned(falcon_graph *g);
+
 void destroy(falcon_graph *g) {
     if (!g) return;
+    if (g->comm) {
+        destroy_partitioned(g);
+        delete g;
+        return;
+    }
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
     for (auto &row : g->execs)
@@ -616,6 +639,8 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
 
 }  // namespace
 
+#include "partition.cuh"
+
 extern "C" {
 
 falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col, const int32_t *w,
@@ -629,7 +654,8 @@ falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, co
         return fail(FALCON_ERR_UNSUPPORTED, "unknown load flags 0x%x", opts->flags);
     falcon_graph *g = new (std::nothrow) falcon_graph();
     if (!g) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
-    falcon_status_t st = load(n, m, row_off, col, w, opts, g);
+    falcon_status_t st = (opts && opts->comm) ? load_partitioned(n, m, row_off, col, w, opts, g)
+                                              : load(n, m, row_off, col, w, opts, g);
     if (st != FALCON_OK) {
         std::string msg = g_last_error;
         destroy(g);
@@ -643,6 +669,66 @@ falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, co
 
 falcon_status_t graph_free(falcon_graph_t *g) {
     destroy(g);
+    return FALCON_OK;
+}
+
+falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi) {
+    if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
+    if (lo) *lo = g->comm ? g->lo : 0;
+    if (hi) *hi = g->comm ? g->hi : g->n;
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_partition(int64_t n, const uint32_t *row_off, int nparts, int64_t *bounds) {
+    if (n < 1 || !row_off || !bounds || nparts < 1) return fail(FALCON_ERR_INVALID_ARG, "bad partition arguments");
+    partition_bounds(n, row_off, nparts, bounds);
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_comm_unique_id(void *id128) {
+    if (!id128) return fail(FALCON_ERR_INVALID_ARG, "id is NULL");
+    NcclApi *nc = nccl_api();
+    if (!nc) return fail(FALCON_ERR_COMM, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    NC(nc->GetUniqueId(&id));
+    memcpy(id128, &id, sizeof id);
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_comm_init(int nranks, int rank, const void *id128, int device, falcon_comm_t **out) {
+    if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return fail(FALCON_ERR_INVALID_ARG, "bad comm arguments");
+    *out = nullptr;
+    NcclApi *nc = nccl_api();
+    if (!nc) return fail(FALCON_ERR_COMM, "libnccl.so.2 could not be loaded");
+    CU(cudaSetDevice(device));
+    falcon_comm *cm = new (std::nothrow) falcon_comm();
+    if (!cm) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    cm->nranks = nranks; cm->rank = rank; cm->device = device;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof id);
+    ncclResult_t r = nc->CommInitRank(&cm->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete cm;
+        return fail(FALCON_ERR_COMM, "ncclCommInitRank: %s", nc->GetErrorString ? nc->GetErrorString(r) : "?");
+    }
+    *out = cm;
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_comm_init_simulated(int nparts, falcon_comm_t **out) {
+    if (!out || nparts < 1 || nparts > 64) return fail(FALCON_ERR_INVALID_ARG, "nparts must be in [1, 64]");
+    falcon_comm *cm = new (std::nothrow) falcon_comm();
+    if (!cm) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    cm->simulated = nparts;
+    cm->nranks = 1;
+    *out = cm;
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_comm_free(falcon_comm_t *cm) {
+    if (!cm) return FALCON_OK;
+    if (cm->nccl && nccl_api() && nccl_api()->CommDestroy) nccl_api()->CommDestroy(cm->nccl);
+    delete cm;
     return FALCON_OK;
 }
 

@@ -1,0 +1,396 @@
+// partition.cuh -- 1-D vertex-partitioned multi-GPU path (DESIGN.md §7,
+// SURVEY.md §8(e)).  Included by falcon.cu (needs falcon_graph, load, run).
+//
+// Part q owns vertices [bounds[q], bounds[q+1]) -- contiguous ranges chosen
+// by EDGE count (binary search on the row_off prefix) -- and stores the CSR
+// rows of its owned vertices only (global column ids), plus a full-length
+// value array: the owned range is authoritative, the rest holds this part's
+// proposals for remote vertices (the "shadow").  A superstep:
+//   1. relax: the single-GPU VERTEX round (k_scan + k_expand_warp) over the
+//      part's rows; MIN lands in the local full-length array;
+//   2. exchange: every owner receives the MIN over all parts of its range
+//      (grouped ncclReduce(ncclMin), one per owner -- volume 4n(P-1)/P per
+//      rank, the reduce-scatter of SURVEY §8(e));
+//   3. apply: owned values improved by a remote proposal are lowered and
+//      marked active;
+//   4. termination: ncclAllReduce(SUM) of the per-part `changed` flag, then
+//      the usual device-side advance -- every part takes the same decision.
+// MIN is associative, commutative and idempotent, so any partition and any
+// exchange schedule reach the same unique fixpoint: results are bit-identical
+// to one GPU (tests: simulated P parts on one device, tests/test_partition*).
+// BFS runs as unit-weight SSSP (hop distance = level).  CC hooks on a
+// replicated label array: local union-find pass, ncclAllReduce(MIN) of the
+// parent array, pointer jumping, until no part hooks (the set of roots only
+// shrinks, so it terminates).
+//
+// "Simulated" communicators run all P parts on the current device in one
+// process with the exchange done by device kernels -- the same partition,
+// relax, apply and termination code -- so the partitioned algorithm is
+// tested on one GPU.  NCCL is bound at run time (dlopen libnccl.so.2): a
+// single-GPU user never needs it.
+#pragma once
+#include <dlfcn.h>
+#include <nccl.h>
+
+struct falcon_comm {
+    int nranks = 1, rank = 0, device = 0;
+    int simulated = 0;            // > 0: number of parts simulated on one device
+    ncclComm_t nccl = nullptr;
+};
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL binding
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi *nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api.h ? &api : nullptr;
+    tried = true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names)
+        if ((api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!api.h) return nullptr;
+#define SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))
+    SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(Reduce); SYM(AllReduce);
+    SYM(Broadcast); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString);
+#undef SYM
+    if (!api.GetUniqueId || !api.CommInitRank || !api.Reduce || !api.AllReduce || !api.Broadcast ||
+        !api.GroupStart || !api.GroupEnd) {
+        api.h = nullptr;
+        return nullptr;
+    }
+    return &api;
+}
+
+#define NC(call)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t _r = (call);                                                                  \
+        if (_r != ncclSuccess)                                                                     \
+            return fail(FALCON_ERR_COMM, "%s: %s", #call,                                          \
+                        nccl_api()->GetErrorString ? nccl_api()->GetErrorString(_r) : "nccl error"); \
+    } while (0)
+
+// ------------------------------------------------------------------ kernels
+// apply: owned values lowered by a remote proposal become active
+__global__ void k_apply_owned(Args a, const int32_t *recv, uint32_t lo, uint32_t cnt) {
+    Ctrl *c = a.ctrl;
+    if (c->done) return;
+    uint32_t *bm_now = bm_of(a, c->iter);
+    bool chg = false;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+        const int32_t r = recv[i];
+        const uint32_t v = lo + i;
+        if (r < a.val[v]) {
+            a.val[v] = r;
+            atomicOr(bm_now + (v >> 5), 1u << (v & 31));
+            chg = true;
+        }
+    }
+    if (__syncthreads_or(chg) && threadIdx.x == 0) c->changed = 1;
+}
+
+// simulated exchange: recv of owner q = MIN over parts of vals[p][lo..hi)
+__global__ void k_sim_reduce_min(const int32_t *const *vals, int nparts, uint32_t lo, uint32_t cnt, int32_t *recv) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+        int32_t m = vals[0][lo + i];
+        for (int p = 1; p < nparts; p++) m = min(m, vals[p][lo + i]);
+        recv[i] = m;
+    }
+}
+
+// simulated all-reduce(MIN) of the full arrays, written back to every part
+__global__ void k_sim_allreduce_min(int32_t *const *vals, int nparts, uint32_t n) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int32_t m = vals[0][i];
+        for (int p = 1; p < nparts; p++) m = min(m, vals[p][i]);
+        for (int p = 0; p < nparts; p++) vals[p][i] = m;
+    }
+}
+
+// simulated all-reduce(SUM) of the parts' `changed` flags
+__global__ void k_sim_sum_changed(Ctrl *const *ctrls, int nparts) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t s = 0;
+    for (int p = 0; p < nparts; p++) s += ctrls[p]->changed;
+    for (int p = 0; p < nparts; p++) ctrls[p]->changed = s;
+}
+
+// ------------------------------------------------------------------ host side
+// Boundaries of nparts contiguous vertex ranges with ~m/nparts arcs each:
+// boundary q is the vertex v >= bounds[q-1] whose prefix row_off[v] is
+// nearest to q*m/nparts (so part sizes deviate by at most one row's degree).
+void partition_bounds(int64_t n, const uint32_t *row_off, int nparts, int64_t *bounds) {
+    const uint64_t m = row_off[n];
+    bounds[0] = 0;
+    for (int q = 1; q < nparts; q++) {
+        const uint64_t target = (m * (uint64_t)q) / (uint64_t)nparts;
+        int64_t lo = bounds[q - 1], hi = n;   // smallest v >= bounds[q-1] with row_off[v] >= target
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (row_off[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        if (lo > bounds[q - 1] && target - row_off[lo - 1] < (uint64_t)row_off[lo] - target) lo--;
+        bounds[q] = lo;
+    }
+    bounds[nparts] = n;
+}
+
+void destroy(falcon_graph *g);
+
+void destroy_partitioned(falcon_graph *g) {
+    for (auto *p : g->parts) {
+        cudaSetDevice(p->device);
+        cudaFree(p->recv);
+        cudaFree(p->cw_unit);
+        p->recv = nullptr;
+        p->cw_unit = nullptr;
+        destroy(p);
+    }
+    g->parts.clear();
+}
+
+// Build the part owning [lo, hi): its rows only, global ids, full n.
+falcon_status_t load_part(int64_t n, const uint32_t *h_row_off, const uint32_t *col, const int32_t *w, int64_t lo,
+                          int64_t hi, int device, void *stream, falcon_graph **out) {
+    std::vector<uint32_t> ro((size_t)n + 1);
+    const uint32_t base = h_row_off[lo], top = h_row_off[hi];
+    for (int64_t v = 0; v <= n; v++) {
+        const uint32_t r = h_row_off[v < lo ? lo : (v > hi ? hi : v)];
+        ro[(size_t)v] = r - base;
+    }
+    falcon_load_opts_t o = {};
+    o.device = device;
+    o.cuda_stream = stream;
+    falcon_graph *p = new (std::nothrow) falcon_graph();
+    if (!p) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    const int64_t mp = (int64_t)(top - base);
+    falcon_status_t st = load(n, mp, ro.data(), col + base, w ? w + base : nullptr, &o, p);
+    if (st != FALCON_OK) { destroy(p); return st; }
+    p->lo = lo; p->hi = hi;
+    CU(dmalloc(&p->recv, (size_t)(hi - lo)));
+    CU(dmalloc(&p->cw_unit, (size_t)(mp ? mp : 1)));
+    if (mp) {
+        int32_t *ones = nullptr;
+        CU(dmalloc(&ones, (size_t)mp));
+        k_fill_i32<<<p->num_sms * 8, BLOCK, 0, p->stream>>>(ones, (uint64_t)mp, 1);
+        k_interleave<<<p->num_sms * 8, BLOCK, 0, p->stream>>>((uint64_t)mp, p->col, ones, p->cw_unit);
+        CU(cudaStreamSynchronize(p->stream));
+        cudaFree(ones);
+    }
+    *out = p;
+    return FALCON_OK;
+}
+
+falcon_status_t load_partitioned(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col, const int32_t *w,
+                                 const falcon_load_opts_t *opts, falcon_graph *g) {
+    falcon_comm *cm = opts->comm;
+    g->comm = cm;
+    g->n = n; g->m = m;
+    const int P = cm->simulated ? cm->simulated : cm->nranks;
+    // host copy of the offsets (the caller's may live on the device)
+    std::vector<uint32_t> h_ro((size_t)n + 1);
+    CU(cudaMemcpy(h_ro.data(), row_off, ((size_t)n + 1) * 4, cudaMemcpyDefault));
+    if (h_ro[0] != 0 || h_ro[(size_t)n] != (uint64_t)m)
+        return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must start at 0 and end at m");
+    for (int64_t v = 0; v < n; v++)
+        if (h_ro[(size_t)v] > h_ro[(size_t)v + 1])
+            return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must be nondecreasing");
+    g->bounds.assign((size_t)P + 1, 0);
+    partition_bounds(n, h_ro.data(), P, g->bounds.data());
+    const int device = cm->simulated ? (opts->device >= 0 ? opts->device : 0) : cm->device;
+    g->device = device;
+    CU(cudaSetDevice(device));
+    for (int q = 0; q < P; q++) {
+        if (!cm->simulated && q != cm->rank) continue;
+        falcon_graph *p = nullptr;
+        falcon_status_t st = load_part(n, h_ro.data(), col, w, g->bounds[q], g->bounds[q + 1], device,
+                                       opts->cuda_stream, &p);
+        if (st != FALCON_OK) return st;
+        g->parts.push_back(p);
+    }
+    g->lo = cm->simulated ? 0 : g->bounds[cm->rank];
+    g->hi = cm->simulated ? n : g->bounds[cm->rank + 1];
+    g->stream = g->parts[0]->stream;
+    return FALCON_OK;
+}
+
+// One partitioned call.  The output is the full n-length array on every rank.
+falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int32_t *out, falcon_stats_t *stats) {
+    if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
+    if (algo != CC && (int64_t)source >= g->n) return fail(FALCON_ERR_INVALID_ARG, "source %u >= n", source);
+    falcon_comm *cm = g->comm;
+    const int P = (int)g->parts.size();
+    NcclApi *nc = cm->simulated ? nullptr : nccl_api();
+    if (!cm->simulated && !nc) return fail(FALCON_ERR_COMM, "libnccl.so.2 could not be loaded");
+    CU(cudaSetDevice(g->device));
+    cudaStream_t s = g->parts[0]->stream;   // simulated parts share the device; order them on one stream
+    const uint32_t cap = (uint32_t)(g->n + 2 > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : g->n + 2);
+    std::vector<Args> args;
+    for (auto *p : g->parts) {
+        p->use_unit = algo == BFS;
+        args.push_back(p->args());
+    }
+    // device pointer tables for the simulated exchange
+    int32_t **d_vals = nullptr;
+    Ctrl **d_ctrls = nullptr;
+    if (cm->simulated) {
+        std::vector<int32_t *> hv;
+        std::vector<Ctrl *> hc;
+        for (auto *p : g->parts) { hv.push_back(p->val); hc.push_back(p->ctrl); }
+        CU(dmalloc(&d_vals, (size_t)P));
+        CU(dmalloc(&d_ctrls, (size_t)P));
+        CU(cudaMemcpyAsync(d_vals, hv.data(), sizeof(int32_t *) * P, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(d_ctrls, hc.data(), sizeof(Ctrl *) * P, cudaMemcpyHostToDevice, s));
+    }
+    CU(cudaEventRecord(g->parts[0]->ev0, s));
+    const int init_algo = algo == CC ? CC : SSSP;
+    for (size_t i = 0; i < g->parts.size(); i++) {
+        falcon_graph *p = g->parts[i];
+        if (init_algo == CC) k_init<CC><<<p->grid_small, BLOCK, 0, s>>>(args[i], 0, cap, 3u * p->cnt_slots, VERTEX, 1);
+        else k_init<SSSP><<<p->grid_small, BLOCK, 0, s>>>(args[i], source, cap, 3u * p->cnt_slots, VERTEX, 1);
+    }
+    CU(cudaGetLastError());
+    int64_t rounds = 0;
+    for (;;) {
+        for (int k = 0; k < HOST_CHECK_EVERY; k++) {
+            rounds++;
+            // 1. relax
+            for (size_t i = 0; i < g->parts.size(); i++) {
+                falcon_graph *p = g->parts[i];
+                if (algo == CC) {
+                    launch_l2(p, k_cc_vertex<BLOCK>, p->grid_cc, s, args[i]);
+                } else {
+                    launch_l2(p, k_scan<SSSP, BLOCK>, p->grid_scan, s, args[i]);
+                    launch_expand_warp<SSSP, VERTEX>(p, s, args[i]);
+                }
+            }
+            // 2.-3. exchange + apply
+            if (algo == CC) {
+                if (cm->simulated) {
+                    k_sim_allreduce_min<<<g->parts[0]->grid_small, BLOCK, 0, s>>>(d_vals, P, (uint32_t)g->n);
+                } else {
+                    NC(nc->AllReduce(g->parts[0]->val, g->parts[0]->val, (size_t)g->n, ncclInt32, ncclMin, cm->nccl, s));
+                }
+                for (size_t i = 0; i < g->parts.size(); i++)
+                    launch_l2(g->parts[i], k_compress, g->parts[i]->grid_small, s, args[i]);
+            } else {
+                if (cm->simulated) {
+                    for (int q = 0; q < P; q++) {
+                        falcon_graph *p = g->parts[(size_t)q];
+                        k_sim_reduce_min<<<p->grid_small, BLOCK, 0, s>>>(d_vals, P, (uint32_t)p->lo,
+                                                                           (uint32_t)(p->hi - p->lo), p->recv);
+                    }
+                } else {
+                    falcon_graph *me = g->parts[0];
+                    NC(nc->GroupStart());
+                    for (int q = 0; q < cm->nranks; q++) {
+                        const int64_t qlo = g->bounds[(size_t)q], qcnt = g->bounds[(size_t)q + 1] - qlo;
+                        if (qcnt == 0) continue;
+                        NC(nc->Reduce(me->val + qlo, me->recv, (size_t)qcnt, ncclInt32, ncclMin, q, cm->nccl, s));
+                    }
+                    NC(nc->GroupEnd());
+                }
+                for (size_t i = 0; i < g->parts.size(); i++) {
+                    falcon_graph *p = g->parts[i];
+                    if (p->hi > p->lo)
+                        k_apply_owned<<<p->grid_small, BLOCK, 0, s>>>(args[i], p->recv, (uint32_t)p->lo,
+                                                                      (uint32_t)(p->hi - p->lo));
+                }
+            }
+            // 4. termination: every part sees the global `changed`
+            if (cm->simulated) {
+                k_sim_sum_changed<<<1, 32, 0, s>>>(d_ctrls, P);
+            } else {
+                NC(nc->AllReduce(&g->parts[0]->ctrl->changed, &g->parts[0]->ctrl->changed, 1, ncclUint32, ncclSum,
+                                 cm->nccl, s));
+            }
+            for (size_t i = 0; i < g->parts.size(); i++) {
+                if (algo == CC)
+                    k_advance<CC, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u);
+                else
+                    k_advance<SSSP, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u);
+            }
+        }
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(g->parts[0]->h_ctrl, g->parts[0]->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (g->parts[0]->h_ctrl->done) break;
+    }
+    for (size_t i = 0; i < g->parts.size(); i++)
+        k_finish<<<1, BLOCK, 0, s>>>(args[i], (uint32_t)g->parts[i]->cnt_slots);
+    // gather: the full array on every rank
+    int32_t *dst = out;
+    int32_t *staging = nullptr;
+    cudaPointerAttributes at;
+    const bool out_on_device = cudaPointerGetAttributes(&at, out) == cudaSuccess &&
+                               (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    if (!out_on_device) {
+        CU(dmalloc(&staging, (size_t)g->n));
+        dst = staging;
+    }
+    if (cm->simulated) {
+        for (auto *p : g->parts)
+            if (p->hi > p->lo)
+                CU(cudaMemcpyAsync(dst + p->lo, p->val + p->lo, (size_t)(p->hi - p->lo) * 4, cudaMemcpyDefault, s));
+    } else {
+        falcon_graph *me = g->parts[0];
+        NC(nc->GroupStart());
+        for (int q = 0; q < cm->nranks; q++) {
+            const int64_t qlo = g->bounds[(size_t)q], qcnt = g->bounds[(size_t)q + 1] - qlo;
+            if (qcnt == 0) continue;
+            NC(nc->Broadcast(me->val + qlo, dst + qlo, (size_t)qcnt, ncclInt32, q, cm->nccl, s));
+        }
+        NC(nc->GroupEnd());
+    }
+    CU(cudaEventRecord(g->parts[0]->ev1, s));
+    if (staging) CU(cudaMemcpyAsync(out, staging, (size_t)g->n * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<Ctrl> hc(g->parts.size());
+    for (size_t i = 0; i < g->parts.size(); i++)
+        CU(cudaMemcpyAsync(&hc[i], g->parts[i]->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (staging) cudaFree(staging);
+    if (d_vals) cudaFree(d_vals);
+    if (d_ctrls) cudaFree(d_ctrls);
+    for (auto *p : g->parts) p->use_unit = false;
+    if (stats) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, g->parts[0]->ev0, g->parts[0]->ev1));
+        memset(stats, 0, sizeof *stats);
+        stats->iterations = hc[0].iter;
+        for (auto &c : hc) {
+            stats->vertices_processed += (int64_t)c.vertices;
+            stats->edges_relaxed += (int64_t)c.edges;
+            stats->updates += (int64_t)c.updates;
+        }
+        stats->kernel_launches = rounds * (algo == CC ? 3 : 4) * (int64_t)g->parts.size() + 2;
+        stats->ms = ms;
+        stats->relax_ms = -1.0;
+    }
+    for (auto &c : hc) {
+        if (c.status == ST_OVERFLOW) return fail(FALCON_ERR_OVERFLOW, "a finite distance would reach FALCON_INF");
+        if (c.status == ST_NOT_CONVERGED) return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", cap);
+    }
+    g_last_error.clear();
+    return FALCON_OK;
+}
+
+}  // namespace

@@ -1,0 +1,62 @@
+"""Partitioned (multi-GPU) algorithm on ONE device: P simulated parts with
+device-side exchange run the same partition / relax / apply / termination
+code as the NCCL ranks; results must equal the oracle bit for bit.  A
+single-rank NCCL communicator exercises the NCCL call path itself."""
+import numpy as np
+import pytest
+import torch
+
+import graphgen as gg
+import oracle
+
+pytestmark = pytest.mark.gpu
+GRAPHS = ["tiny", "rand-s", "rmat-s", "grid-s"]
+_cache = {}
+
+
+def _g(name):
+    if name not in _cache:
+        _cache[name] = gg.config(name)
+    return _cache[name]
+
+
+@pytest.mark.parametrize("name", GRAPHS)
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("algo", ["sssp", "bfs", "cc"])
+def test_simulated_partition_parity(gpu_lib, name, P, algo):
+    fb = gpu_lib
+    G = _g(name)
+    comm = fb.falcon_comm_init_simulated(P)
+    g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, comm=comm)
+    assert fb.graph_owned_range(g) == (0, G.n)
+    out = np.empty(G.n, np.int32)
+    st = fb.run(g, algo, "vertex", out, G.source)
+    exp = oracle.run(algo, G)
+    assert np.array_equal(out, exp), f"{name}/P={P}/{algo}: {np.flatnonzero(out != exp)[:10]}"
+    assert st.iterations >= 1
+
+
+def test_simulated_partition_device_output_and_repeat(gpu_lib):
+    fb = gpu_lib
+    G = _g("rmat-s")
+    comm = fb.falcon_comm_init_simulated(4)
+    g = fb.graph_load_csr(G.n, G.m, torch.from_numpy(G.row_off).cuda(), torch.from_numpy(G.col).cuda(),
+                          torch.from_numpy(G.w).cuda(), device=0, comm=comm)
+    out = torch.empty(G.n, dtype=torch.int32, device="cuda")
+    for algo in ("sssp", "bfs", "cc"):
+        for _ in range(2):
+            fb.run(g, algo, "vertex", out, G.source)
+            assert np.array_equal(out.cpu().numpy(), oracle.run(algo, G))
+
+
+def test_nccl_single_rank(gpu_lib):
+    fb = gpu_lib
+    G = _g("rand-s")
+    uid = fb.falcon_comm_unique_id()
+    comm = fb.falcon_comm_init(1, 0, uid, 0)
+    g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, comm=comm)
+    assert fb.graph_owned_range(g) == (0, G.n)
+    out = np.empty(G.n, np.int32)
+    for algo in ("sssp", "bfs", "cc"):
+        fb.run(g, algo, "vertex", out, G.source)
+        assert np.array_equal(out, oracle.run(algo, G))
