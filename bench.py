@@ -50,6 +50,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-max-steps", type=int, default=3)
+    ap.add_argument("--mode", default="replica", choices=["replica", "partition"],
+                    help="N>1: replica = one independent graph per GPU (PAPER.md:1587-1597 'parallel "
+                         "sections', weak scaling); partition = one graph 1-D vertex-partitioned over the "
+                         "GPUs with NCCL exchange (SURVEY.md §8(e), strong scaling)")
+    ap.add_argument("--simulate", type=int, default=0,
+                    help="partition mode on ONE GPU with this many simulated parts (device-side exchange)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -231,8 +237,10 @@ def main():
     algos = [a for a in args.algos.split(",") if a]
     styles = [s for s in args.styles.split(",") if s]
 
-    # Workload: the BASELINE.json config; replica r uses seed + r (weak scaling).
-    if world > 1 and rank > 0:
+    partition = args.mode == "partition" or args.simulate > 0
+    # Workload: the BASELINE.json config; replica r uses seed + r (weak scaling);
+    # partition mode: the same graph on every rank (each keeps its rows).
+    if world > 1 and rank > 0 and not partition:
         base = gg.CONFIGS[args.config]
         G = {"rand-25M": lambda: gg.er(25_000_000, 100_000_000, 25 + rank, name="rand-25M"),
              "rmat-10M": lambda: gg.rmat(10_000_000, 100_000_000, 10 + rank, name="rmat-10M"),
@@ -240,9 +248,20 @@ def main():
     else:
         G = gg.config(args.config)
     stream = torch.cuda.current_stream()
-    g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream, flags=fb.LOAD_BUILD_COO)
+    comm = None
+    if partition:
+        if args.simulate > 0:
+            comm = fb.falcon_comm_init_simulated(args.simulate)
+        else:
+            obj = [fb.falcon_comm_unique_id() if rank == 0 else None]
+            if dist:
+                dist.broadcast_object_list(obj, src=0)
+            comm = fb.falcon_comm_init(world, rank, obj[0], local)
+        styles = ["vertex"]   # the partitioned path runs the VERTEX round on every part
+    g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream,
+                          flags=0 if partition else fb.LOAD_BUILD_COO, comm=comm)
     out = torch.empty(G.n, dtype=torch.int32, device="cuda")
-    runs = [(a, s) for a in algos for s in styles]
+    runs = [(a, s) for a in algos for s in styles if s != "delta" or a == "sssp"]   # DELTA is SSSP-only
 
     def step(collect=None):
         launches = 0
@@ -284,26 +303,37 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * units_per_step * args.steps / (ms_total * 1e-3) / 1e9
+    replicas = world if not partition else 1   # partition: one shared graph (strong scaling)
+    value = replicas * units_per_step * args.steps / (ms_total * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel: one profiled step (host-driven loop,
     # CUDA events around every relax launch on the library stream)
-    fb.falcon_set_profiling(g, True)
-    prof = {}
-    step(prof)
-    fb.falcon_set_profiling(g, False)
     hbm, hbm_src = peaks()
-    shares = {k: v[0]["relax_ms"] for k, v in prof.items()}
-    dom = max(shares, key=shares.get)
-    dst = prof[dom][0]
-    bytes_dom = algorithmic_bytes(dom[0], dom[1], dst, G.n, G.m)
-    achieved = bytes_dom / (dst["relax_ms"] * 1e-3) / 1e9
-    key = f"{dom[0]}/{dom[1]}"
-    traffic = ncu_traffic(key)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": f"relax {key}", "peak_source": hbm_src,
-                "relax_ms": dst["relax_ms"], "relax_launches": dst["relax_launches"],
-                "algorithmic_bytes": bytes_dom, "share_of_step": dst["relax_ms"] / ms_step}
+    prof = {}
+    if not partition:
+        fb.falcon_set_profiling(g, True)
+        step(prof)
+        fb.falcon_set_profiling(g, False)
+        shares = {k: v[0]["relax_ms"] for k, v in prof.items()}
+        dom = max(shares, key=shares.get)
+        dst = prof[dom][0]
+        bytes_dom = algorithmic_bytes(dom[0], dom[1], dst, G.n, G.m)
+        achieved = bytes_dom / (dst["relax_ms"] * 1e-3) / 1e9
+        key = f"{dom[0]}/{dom[1]}"
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": ncu_traffic(key), "kernel": f"relax {key}", "peak_source": hbm_src,
+                    "relax_ms": dst["relax_ms"], "relax_launches": dst["relax_launches"],
+                    "algorithmic_bytes": bytes_dom, "share_of_step": dst["relax_ms"] / ms_step}
+    else:   # partitioned: the whole superstep loop (relax + exchange) of the slowest algorithm
+        worst = max(per_run, key=lambda k: statistics.median(x["ms"] for x in per_run[k]))
+        x = per_run[worst][-1]
+        ms = statistics.median(y["ms"] for y in per_run[worst])
+        bytes_dom = algorithmic_bytes(worst[0], "vertex", x, G.n, G.m)
+        achieved = bytes_dom / (ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm * (world if not args.simulate else 1),
+                    "unit": "GB/s", "frac": achieved / (hbm * (world if not args.simulate else 1)), "traffic": None,
+                    "kernel": f"partitioned superstep loop {worst[0]} (relax + exchange, all parts)",
+                    "peak_source": hbm_src + (" x ranks" if world > 1 else ""), "algorithmic_bytes": bytes_dom}
 
     breakdown = {}
     for (a, s), lst in per_run.items():
@@ -314,7 +344,7 @@ def main():
         breakdown[f"{a}/{s}"] = {"ms": ms, "gteps": mc[a] / (ms * 1e-3) / 1e9, "iterations": x["iterations"],
                                  "edges_relaxed": x["edges_relaxed"], "updates": x["updates"],
                                  "relax_ms": p["relax_ms"], "alg_GBps_relax": bts / (p["relax_ms"] * 1e-3) / 1e9
-                                 if p["relax_ms"] > 0 else None,
+                                 if p["relax_ms"] and p["relax_ms"] > 0 else None,
                                  "one_pass_eff": ((12 if a == "sssp" else 8) * G.m + 8 * G.n) / (ms * 1e-3) / 1e9 / hbm}
 
     # ---- e2e through the C ABI with HOST buffers (H2D + D2H inside the timed region)
@@ -326,7 +356,7 @@ def main():
         e_steps = max(1, min(args.steps, 3))
 
         def e2e_step():
-            gh = fb.graph_load_csr(G.n, G.m, h_ro, h_col, h_w, device=local, stream=stream)
+            gh = fb.graph_load_csr(G.n, G.m, h_ro, h_col, h_w, device=local, stream=stream, comm=comm)
             for a, s in runs:
                 fb.run(gh, a, s, h_out, G.source)
             fb.graph_free(gh)
@@ -346,7 +376,7 @@ def main():
             t = torch.tensor([ems], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": world * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",
+        e2e = {"value": replicas * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": 4 * (G.n + 1) + 8 * G.m, "d2h_bytes_per_step": 4 * G.n * len(runs),
                "steps": e_steps, "ms_per_step": ems / e_steps}
 
@@ -360,11 +390,13 @@ def main():
     if rank == 0:
         line = {"metric": "SSSP/BFS/CC GTEPS (aggregate over runs per step)", "value": value, "unit": "GTEPS",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-                "data": "synthetic",
+                "higher_is_better": True, "scaling": "strong" if partition else "weak", "vs_baseline": None,
+                "dtype": "int32", "data": "synthetic",
                 "config": {"workload": args.config, "n": G.n, "m": G.m, "source": G.source, "algos": algos,
                            "styles": styles, "runs_per_step": len(runs),
-                           "parallelism": "replicas" if world > 1 else "single",
+                           "parallelism": (f"partition{world}" + (f" (simulated {args.simulate} parts on 1 GPU)"
+                                                                   if args.simulate else "")) if partition
+                           else ("replicas" if world > 1 else "single"),
                            "l2": "inputs larger than L2 (CSR+COO %.2f GB vs 126 MB L2); each run re-initialises "
                                  "its value array" % ((4 * (G.n + 1) + 12 * G.m) / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -91,7 +91,8 @@ struct falcon_graph {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> pev;
     int variant = 0;                     // FALCON_EXPAND_VARIANT
-    bool persist = true;                 // queue styles run all rounds in one cooperative kernel (FALCON_PERSIST=0: per-round launches)
+    bool persist = false;                // queue styles: small rounds in one cooperative kernel (FALCON_PERSIST=1: on)
+    uint32_t persist_max = 65536;        // ... while the frontier has at most this many items (FALCON_PERSIST_MAX)
     bool l2_window = false;              // persisting L2 access-policy window on val[]
     cudaAccessPolicyWindow apw = {};
 
@@ -204,12 +205,22 @@ struct Round {
             launch_expand_warp<ALGO, VERTEX>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == DELTA) {
+            if (g->persist) {   // small rounds inside one cooperative kernel
+                launch_coop(g, k_persist<SSSP, DELTA, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div, g->persist_max);
+                launches++;
+            }
             launch_l2(g, k_scan_far<BLOCK>, g->grid_pull, s, a);
             launches++;
             if (tr) tr->mark(s, "scan_far", 0);
             launch_expand_warp<ALGO, DELTA>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == WORKLIST) {
+            if (g->persist) {
+                launch_coop(g, k_persist<ALGO, WORKLIST, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div,
+                            g->persist_max);
+                launches++;
+                if (tr) tr->mark(s, "persist", 0);
+            }
             launch_expand_warp<ALGO, WORKLIST>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else {
@@ -306,7 +317,11 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
     k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
     k_scan_add<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(g->rin_off, n + 1, tiles);
     CU(cudaMemcpyAsync(cursor, g->rin_off, (n + 1) * 4, cudaMemcpyDeviceToDevice, s));
-    if (m) k_rev_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->col, cursor, g->rin_col);
+    if (m) {
+        falcon_status_t st = ensure_src(g);
+        if (st != FALCON_OK) return st;
+        k_rev_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->src, g->col, cursor, g->rin_col);
+    }
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));
     cudaFree(cursor);
@@ -366,7 +381,7 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
 
     double relax_ms = -1.0;
     int64_t relax_launches = 0;
-    int64_t cc_passes = 0, cc_launches = 0, persist_launches = 0;
+    int64_t cc_passes = 0, cc_launches = 0;
     if (algo == CC) {
         // Fixed pass sequence (no fixpoint loop): union-find hooking is exact
         // after one pass over the arcs (cc.cuh).
@@ -407,24 +422,6 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
                 CU(cudaEventElapsedTime(&ms, tr.marks[i - 1].ev, tr.marks[i].ev));
                 if (tr.marks[i].kind == 0) { relax_ms += ms; relax_launches++; }
             }
-        }
-    } else if (g->persist && (style == WORKLIST || style == DELTA)) {
-        // all rounds inside one cooperative kernel (k_persist)
-        Tracer tr{g};
-        if (g->profiling) tr.mark(s, "begin", 1);
-        cudaError_t e;
-        if (algo == BFS) e = launch_coop(g, k_persist<BFS, WORKLIST, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div);
-        else if (style == DELTA) e = launch_coop(g, k_persist<SSSP, DELTA, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div);
-        else e = launch_coop(g, k_persist<SSSP, WORKLIST, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div);
-        if (e != cudaSuccess) return fail(FALCON_ERR_CUDA, "cooperative launch of k_persist: %s", cudaGetErrorString(e));
-        persist_launches = 1;
-        if (g->profiling) {
-            tr.mark(s, "persist", 0);
-            float ms = 0.f;
-            CU(cudaEventSynchronize(tr.marks[1].ev));
-            CU(cudaEventElapsedTime(&ms, tr.marks[0].ev, tr.marks[1].ev));
-            relax_ms = ms;
-            relax_launches = 1;
         }
     } else if (!g->profiling) {
         falcon_status_t st = build_graph(g, algo, style);
@@ -483,7 +480,7 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
         stats->vertices_processed = (int64_t)c.vertices;
         stats->edges_relaxed = (int64_t)c.edges;
         stats->updates = (int64_t)c.updates;
-        stats->kernel_launches = (int64_t)c.launches + cc_launches + persist_launches;
+        stats->kernel_launches = (int64_t)c.launches + cc_launches;
         stats->ms = ms;
         stats->relax_ms = relax_ms;
         stats->relax_launches = relax_launches;
@@ -577,7 +574,9 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
         if (o2 < occ_p) occ_p = o2;
     }
     const char *pe = getenv("FALCON_PERSIST");
-    g->persist = !(pe && pe[0] == '0') && occ_p > 0;
+    g->persist = (pe && pe[0] == '1') && occ_p > 0;   // measured: no faster than per-round graph launches
+    const char *pm = getenv("FALCON_PERSIST_MAX");
+    if (pm) g->persist_max = (uint32_t)atoll(pm);
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK, EDGE_QP>, BLOCK, 0));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scan<SSSP, BLOCK>, BLOCK, 0));
     auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };

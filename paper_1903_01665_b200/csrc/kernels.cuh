@@ -862,13 +862,16 @@ __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, u
 }
 
 // ------------------------------------------------------------------ persistent rounds
-// Queue styles (WORKLIST, DELTA) run ALL their rounds inside one cooperative
-// kernel: a round's expansion, then a grid barrier whose last arriving CTA
-// performs the advance (the same advance_step as k_advance) and releases the
-// others.  A round then costs one barrier (~µs) instead of two kernel launches
-// -- it is what makes the thousands of small rounds of road-like graphs
-// and Δ-stepping buckets affordable.  Data written earlier
-// in the kernel is read with L1-bypassing loads (COHERENT).
+// Optional (FALCON_PERSIST=1): queue styles (WORKLIST, DELTA) run their SMALL
+// rounds (frontier <= max_items) inside one cooperative kernel: a round's
+// expansion, then a grid barrier whose last arriving CTA performs the advance
+// (the same advance_step as k_advance) and releases the others.  Large rounds
+// leave the kernel and run as one launch per round; the CUDA-graph round body
+// is [k_persist, round kernels, k_advance].  Data written earlier in the
+// kernel is read with L1-bypassing loads.  Measured on B200 a persistent
+// round costs about as much as a graph-launched one (~11-13 µs on the road
+// grid: the round is bound by its chain of dependent memory accesses, the
+// barrier is ~2.7 µs, tools/barrier_probe.cu), so it is off by default.
 __device__ __forceinline__ uint32_t ldv(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
 template <int ALGO, int STYLE>
@@ -892,18 +895,22 @@ __device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32
 }
 
 template <int ALGO, int STYLE, int B, int U>
-__global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div) {
+__global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div, uint32_t max_items) {
     static_assert(STYLE == WORKLIST || STYLE == DELTA, "persistent rounds are for the queue styles");
     __shared__ uint32_t s_q[B / 32][512];
     Ctrl *c = a.ctrl;
     RoundAcc acc;
     for (;;) {
-        if (ldv(&c->done)) break;   // uniform: every CTA reads after the same barrier
+        // uniform exits (every CTA reads the same state after the same barrier):
+        // done, or a frontier large enough for the one-launch-per-round kernels
+        if (ldv(&c->done)) break;
+        const bool scan = STYLE == DELTA && ldv(&c->mode) == MODE_SCAN;
+        if (!scan && ldv(&c->in_len) > max_items) break;
         const uint32_t iter = ldv(&c->iter), sel = ldv(&c->sel);
         const uint32_t thr = STYLE == DELTA ? ldv(&c->thr) : 0xffffffffu;
         const uint32_t *in = sel ? a.fr1 : a.fr0;
         uint32_t *out = sel ? a.fr0 : a.fr1;
-        if (STYLE == DELTA && ldv(&c->mode) == MODE_SCAN)
+        if (scan)
             scan_far_round<true>(a, c, iter, thr, out, acc.nv);
         else
             expand_round<ALGO, STYLE, U, true>(a, c, iter, thr, in, out, ldv(&c->in_len), false,
@@ -994,11 +1001,13 @@ __global__ void k_scan_add(uint32_t *x, uint64_t len, const uint32_t *tile_sums)
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < len) x[i] += tile_sums[i / 1024];
 }
-__global__ void k_rev_scatter(uint32_t n, const uint32_t *row_off, const uint32_t *col, uint32_t *cursor,
+// arc-parallel scatter of the COO arcs into the in-rows (in-row order is
+// arbitrary: BFS levels and CC labels do not depend on it)
+__global__ void k_rev_scatter(uint64_t m, const uint32_t *src, const uint32_t *col, uint32_t *cursor,
                               uint32_t *rin_col) {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride)
-        for (uint32_t e = row_off[u]; e < row_off[u + 1]; e++) rin_col[atomicAdd(cursor + col[e], 1u)] = u;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride)
+        rin_col[atomicAdd(cursor + col[e], 1u)] = src[e];
 }
 
 __global__ void k_fill_i32(int32_t *p, uint64_t len, int32_t x) {
@@ -1006,17 +1015,13 @@ __global__ void k_fill_i32(int32_t *p, uint64_t len, int32_t x) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) p[i] = x;
 }
 
-// COO sources in CSR order: src[e] = the row containing arc e (binary search
-// on row_off: largest u with row_off[u] <= e).
+// COO sources in CSR order: src[e] = u for every arc of row u (row-parallel
+// fill; rows are short except RMAT hubs, which one thread writes in µs).
 __global__ void k_build_src(uint32_t n, uint32_t m, const uint32_t *row_off, uint32_t *src) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        uint32_t lo = 0, hi = n - 1;
-        while (lo < hi) {
-            const uint32_t mid = lo + ((hi - lo + 1) >> 1);
-            if (row_off[mid] <= (uint32_t)e) lo = mid; else hi = mid - 1;
-        }
-        src[e] = lo;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+        const uint32_t e1 = row_off[u + 1];
+        for (uint32_t e = row_off[u]; e < e1; e++) src[e] = u;
     }
 }
 
