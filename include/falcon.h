@@ -175,6 +175,22 @@ FALCON_API falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, in
  * Errors: INVALID_ARG (g NULL or delta < 0). */
 FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
 
+/* Tuning options of a loaded graph (results never depend on them; they pick
+ * the data layout and schedule).  name / value:
+ *   "block_bytes"  value-array bytes per destination block of the SSSP arc
+ *                  layout (default 24 MiB, env FALCON_BLOCK_MB; 0 = no blocking)
+ *   "dense_div"    a round is dense (bitmap-driven, in vertex order; SSSP
+ *                  over the blocked layout) when its frontier exceeds
+ *                  n / dense_div (default 64, env FALCON_DENSE_DIV; 0 = never)
+ *   "pull_div"     BFS VERTEX runs bottom-up while the frontier exceeds
+ *                  n / pull_div (default 16; 0 = never)
+ *   "persist"      queue styles run small rounds in one cooperative kernel (0/1)
+ *   "persist_max"  ... while the frontier holds at most this many items
+ * Changing an option drops the cached CUDA graphs (and, for block_bytes, the
+ * blocked layout); they are rebuilt on the next call.
+ * Errors: INVALID_ARG (g/name NULL, value out of range), UNSUPPORTED (unknown name). */
+FALCON_API falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t value);
+
 /* Profiling mode (off by default): when on, the fixpoint loop is driven from
  * the host and every relax-kernel launch is bracketed by CUDA events, filling
  * falcon_stats_t.relax_ms / relax_launches.  Results are identical. */

@@ -6,7 +6,7 @@ every call raises.  Arrays may be numpy arrays (host) or torch tensors (host
 or CUDA); PyTorch is used only for device memory and streams.
 
 Names follow the C ABI: graph_load_csr, graph_free, graph_info, graph_owned_range,
-falcon_sssp, falcon_bfs, falcon_cc, falcon_set_profiling, falcon_set_delta,
+falcon_sssp, falcon_bfs, falcon_cc, falcon_set_profiling, falcon_set_delta, falcon_set_option,
 falcon_partition, falcon_comm_unique_id, falcon_comm_init,
 falcon_comm_init_simulated, falcon_comm_free, falcon_last_error, falcon_version.
 """
@@ -16,7 +16,7 @@ import ctypes
 import os
 
 __all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "falcon_sssp", "falcon_bfs", "falcon_cc",
-           "falcon_set_profiling", "falcon_set_delta", "falcon_partition", "falcon_comm_unique_id",
+           "falcon_set_profiling", "falcon_set_delta", "falcon_set_option", "falcon_partition", "falcon_comm_unique_id",
            "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_free", "graph_owned_range", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
 
@@ -76,6 +76,8 @@ def load(build_if_missing: bool = False):
     lib.falcon_set_profiling.argtypes = [p, ctypes.c_int]
     lib.falcon_set_delta.argtypes = [p, ctypes.c_int32]
     lib.falcon_set_delta.restype = st
+    lib.falcon_set_option.argtypes = [p, ctypes.c_char_p, i64]
+    lib.falcon_set_option.restype = st
     lib.falcon_partition.argtypes = [i64, p, ctypes.c_int, p]
     lib.falcon_comm_unique_id.argtypes = [p]
     lib.falcon_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, p, ctypes.c_int, ctypes.POINTER(p)]
@@ -263,6 +265,12 @@ def falcon_set_profiling(g: Graph, enable: bool):
 def falcon_set_delta(g: Graph, delta: int):
     """Bucket width of the DELTA style (0 = auto: max(1, average weight))."""
     _check(load().falcon_set_delta(g.handle, int(delta)))
+
+
+def falcon_set_option(g: Graph, name: str, value: int):
+    """Tuning option of a loaded graph (include/falcon.h: block_bytes, dense_div,
+    pull_div, persist, persist_max).  Results never depend on it."""
+    _check(load().falcon_set_option(g.handle, name.encode(), int(value)))
 
 
 def falcon_last_error() -> str:

@@ -72,6 +72,11 @@ struct falcon_graph {
     uint32_t *row_off = nullptr, *col = nullptr, *src = nullptr;
     int32_t *w = nullptr;
     uint2 *cw = nullptr;
+    uint32_t *rowb = nullptr, *srcb = nullptr;   // destination-blocked layout (SSSP), built lazily
+    uint2 *cwb = nullptr;
+    uint32_t nblk = 1, bsz = 0;
+    size_t blk_bytes = 24u << 20;        // value-array bytes per block (FALCON_BLOCK_MB)
+    uint32_t dense_div = 64;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV)
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     int32_t *val = nullptr;
@@ -82,7 +87,7 @@ struct falcon_graph {
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_persist = 0, grid_expand_fr = 0, grid_scan = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    int grid_persist = 0, grid_expand_fr = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
     cudaGraph_t graphs[3][4] = {};
     cudaGraphExec_t execs[3][4] = {};
     int32_t delta = 0;                   // DELTA bucket width (0 = auto: max(1, average weight))
@@ -110,6 +115,12 @@ struct falcon_graph {
         a.n = (uint32_t)n; a.m = (uint32_t)m; a.nwords = nwords;
         a.row_off = row_off; a.col = col; a.w = w; a.cw = use_unit ? cw_unit : cw; a.src = src;
         a.rin_off = rin_off; a.rin_col = rin_col;
+        const bool blk = rowb && !use_unit;
+        a.nblk = blk ? nblk : 1u;
+        a.rowb = blk ? rowb : row_off;
+        a.cwb = blk ? cwb : a.cw;
+        a.srcb = blk ? srcb : src;
+        a.dense_div = dense_div;
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
@@ -194,9 +205,6 @@ struct Round {
         int launches = 0;
         if (tr) tr->mark(s, "begin", 1);
         if (STYLE == VERTEX) {
-            launch_l2(g, k_scan<ALGO, BLOCK>, g->grid_scan, s, a);
-            launches++;
-            if (tr) tr->mark(s, "scan", 0);
             if (ALGO == BFS) {
                 launch_l2(g, k_pull<BLOCK>, g->grid_pull, s, a);
                 launches++;
@@ -229,7 +237,8 @@ struct Round {
         }
         launches++;
         launches++;
-        k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n, g->pull_div);
+        k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n, g->pull_div,
+                                                 g->dense_div);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
     }
@@ -300,6 +309,40 @@ falcon_status_t ensure_src(falcon_graph *g) {
     return FALCON_OK;
 }
 
+// Destination-blocked copy of the arcs for SSSP, built once
+// on the device: nblk = ceil(4n / blk_bytes) blocks (1 = not needed).
+falcon_status_t ensure_blocked(falcon_graph *g) {
+    if (g->rowb || g->m == 0) return FALCON_OK;
+    const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
+    uint64_t K = (4 * n + g->blk_bytes - 1) / (g->blk_bytes ? g->blk_bytes : 1);
+    if (K > MAX_BLK) K = MAX_BLK;
+    while (K > 1 && K * (n + 1) >= (1ull << 32)) K--;
+    if (K <= 1) return FALCON_OK;
+    const uint32_t bsz = (uint32_t)(((n + K - 1) / K + 31) / 32 * 32);
+    K = (n + bsz - 1) / bsz;
+    if (K <= 1) return FALCON_OK;
+    cudaStream_t s = g->stream;
+    const uint64_t len = K * (n + 1);
+    const uint32_t ntiles = (uint32_t)((len + 1023) / 1024);
+    uint32_t *tiles = nullptr;
+    CU(dmalloc(&g->rowb, len));
+    CU(dmalloc(&g->cwb, m));
+    CU(dmalloc(&g->srcb, m));
+    CU(dmalloc(&tiles, ntiles));
+    k_blk_count<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->col, bsz, (uint32_t)K, g->rowb);
+    k_scan_local<<<ntiles, 256, 0, s>>>(g->rowb, len, tiles);
+    k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
+    k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(g->rowb, len, tiles);
+    k_blk_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->cw, bsz, (uint32_t)K, g->rowb, g->cwb,
+                                                   g->srcb);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s));
+    cudaFree(tiles);
+    g->nblk = (uint32_t)K;
+    g->bsz = bsz;
+    return FALCON_OK;
+}
+
 // Reverse CSR for bottom-up BFS (built once, on the device).
 falcon_status_t ensure_reverse(falcon_graph *g) {
     if (g->rin_off) return FALCON_OK;
@@ -331,6 +374,17 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
 
 falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int32_t *out, falcon_stats_t *stats);
 
+// Drop the cached CUDA graphs (they bake in the launch arguments).
+void drop_graphs(falcon_graph *g) {
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    for (auto &row : g->execs)
+        for (auto &x : row)
+            if (x) { cudaGraphExecDestroy(x); x = nullptr; }
+    for (auto &row : g->graphs)
+        for (auto &x : row)
+            if (x) { cudaGraphDestroy(x); x = nullptr; }
+}
+
 falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out, falcon_stats_t *stats) {
     if (g && g->comm) {
         if (style < 0 || style > 3) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
@@ -345,6 +399,10 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     CU(cudaSetDevice(g->device));
     if (style == EDGE) {
         falcon_status_t st = ensure_src(g);
+        if (st != FALCON_OK) return st;
+    }
+    if (algo == SSSP) {
+        falcon_status_t st = ensure_blocked(g);
         if (st != FALCON_OK) return st;
     }
     if ((algo == BFS && style == VERTEX && g->pull_div) || (algo == CC && style == WORKLIST)) {
@@ -513,6 +571,7 @@ void destroy(falcon_graph *g) {
     if (g->ev1) cudaEventDestroy(g->ev1);
     cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->cw); cudaFree(g->src);
     cudaFree(g->rin_off); cudaFree(g->rin_col);
+    cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb);
     cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1);
     cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
@@ -560,7 +619,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (m) k_interleave<<<g->num_sms * 8, BLOCK, 0, s>>>((uint64_t)m, g->col, g->w, g->cw);
 
     // grid sizes: a multiple of the SM count x resident CTAs, capped by the work
-    int occ_f = 0, occ_e = 0, occ_s = 0, occ_p = 0;
+    int occ_f = 0, occ_e = 0, occ_p = 0;
     const char *var = getenv("FALCON_EXPAND_VARIANT");
     g->variant = var ? atoi(var) : 0;
     static const int var_minb[5] = {MINB, 8, 2, 3, 6};
@@ -578,20 +637,20 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     const char *pm = getenv("FALCON_PERSIST_MAX");
     if (pm) g->persist_max = (uint32_t)atoll(pm);
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK, EDGE_QP>, BLOCK, 0));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scan<SSSP, BLOCK>, BLOCK, 0));
     auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };
     auto full = [&](int occ) { return (int64_t)g->num_sms * (occ > 0 ? occ : 1); };
     g->grid_persist = (int)full(occ_p);
     g->grid_expand_fr = clampg((n + BLOCK - 1) / BLOCK, full(occ_f));
     g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP - 1) / (BLOCK * EDGE_QP), full(occ_e));
-    g->grid_scan = clampg((g->nwords + 4 * BLOCK - 1) / (4 * BLOCK), (int64_t)g->num_sms * 4);
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     g->grid_cc = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
+    if (const char *bmb = getenv("FALCON_BLOCK_MB")) g->blk_bytes = (size_t)atoll(bmb) << 20;   // 0: no blocking
+    if (const char *dd = getenv("FALCON_DENSE_DIV")) g->dense_div = (uint32_t)atoi(dd);        // 0: never dense
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_persist;
-    for (int gsz : {g->grid_expand_fr, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull, g->grid_scan})
+    for (int gsz : {g->grid_expand_fr, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull})
         if (gsz > slots) slots = gsz;
     g->cnt_slots = slots;
     CU(dmalloc(&g->cnt, 3 * (size_t)slots));
@@ -756,6 +815,34 @@ falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta) {
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (delta < 0) return fail(FALCON_ERR_INVALID_ARG, "delta must be >= 0 (0 = auto)");
     g->delta = delta;
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t value) {
+    if (!g || !name) return fail(FALCON_ERR_INVALID_ARG, "graph or option name is NULL");
+    if (value < 0 || value > 0xffffffffll) return fail(FALCON_ERR_INVALID_ARG, "option value out of range");
+    std::vector<falcon_graph *> targets;
+    if (g->comm) targets = g->parts; else targets.push_back(g);
+    for (falcon_graph *t : targets) {
+        if (!strcmp(name, "block_bytes")) {
+            if (t->stream) cudaStreamSynchronize(t->stream);
+            cudaFree(t->rowb); cudaFree(t->cwb); cudaFree(t->srcb);
+            t->rowb = nullptr; t->cwb = nullptr; t->srcb = nullptr; t->nblk = 1; t->bsz = 0;
+            t->blk_bytes = (size_t)value;
+        } else if (!strcmp(name, "dense_div")) {
+            t->dense_div = (uint32_t)value;
+        } else if (!strcmp(name, "pull_div")) {
+            t->pull_div = (uint32_t)value;
+        } else if (!strcmp(name, "persist")) {
+            if (value && t->grid_persist <= 0) return fail(FALCON_ERR_UNSUPPORTED, "cooperative launch unavailable");
+            t->persist = value != 0;
+        } else if (!strcmp(name, "persist_max")) {
+            t->persist_max = (uint32_t)value;
+        } else {
+            return fail(FALCON_ERR_UNSUPPORTED, "unknown option '%s'", name);
+        }
+        drop_graphs(t);
+    }
     return FALCON_OK;
 }
 

@@ -41,7 +41,7 @@ enum DevStatus : int { ST_OK = 0, ST_OVERFLOW = 5, ST_NOT_CONVERGED = 6 };
 // copy of PAPER.md:1682-1684 / SPEC.md:370).
 struct Ctrl {
     uint32_t iter;        // current round, 1-based
-    uint32_t in_len;      // items in the input frontier (VERTEX: built by k_scan)
+    uint32_t in_len;      // items in the input frontier (queue styles)
     uint32_t out_len;     // WORKLIST: items appended to the output frontier
     uint32_t changed;     // VERTEX/EDGE: some value decreased this round
     uint32_t cap;         // round cap (n + 2)
@@ -58,6 +58,7 @@ struct Ctrl {
     uint32_t mode;        // DELTA: MODE_NEAR (relax the near queue) / MODE_SCAN (refill from far)
     uint32_t bar_arrive;  // persistent kernel: CTAs arrived at the grid barrier
     uint32_t bar_gen;     // persistent kernel: barrier generation
+    uint32_t blk;         // this round expands over the destination-blocked layout (dense rounds)
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
     unsigned long long edges;
@@ -71,6 +72,15 @@ struct Args {
     const int32_t *w;          // [m]
     const uint2 *cw;           // [m] (col, w) interleaved: SSSP reads one 8-byte word per arc
     const uint32_t *src;       // [m] COO sources (CSR order), EDGE style only
+    // destination-blocked layout (SSSP): the arcs of block k
+    // (targets in [k*bsz, (k+1)*bsz)) form their own CSR; rowb[k*(n+1)+u] is
+    // the first arc of row u in block k.  nblk == 1: rowb/cwb/srcb alias
+    // row_off/cw/src.
+    const uint32_t *rowb;      // [nblk*(n+1)]
+    const uint2 *cwb;          // [m]
+    const uint32_t *srcb;      // [m] EDGE style
+    uint32_t nblk;
+    uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
@@ -173,7 +183,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t &total,
 
 template <int B>
 __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long nv, unsigned long long ne,
-                                               unsigned long long nu, bool chg, bool ovf, bool count_found = false) {
+                                               unsigned long long nu, bool chg, bool ovf) {
     __shared__ unsigned long long s_red[3][B / 32];
     __shared__ int s_flags;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -194,7 +204,7 @@ __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long
         for (int i = 0; i < B / 32; i++) { t0 += s_red[0][i]; t1 += s_red[1][i]; t2 += s_red[2][i]; }
         unsigned long long *c = a.cnt + 3ull * blockIdx.x;   // this CTA's private slot: no atomics
         c[0] += t0; c[1] += t1; c[2] += t2;
-        if (count_found && t2) atomicAdd(&a.ctrl->found, (uint32_t)t2);
+        if (t2) atomicAdd(&a.ctrl->found, (uint32_t)(t2 < 0xffffffffull ? t2 : 0xffffffffull));   // density heuristics
         if (s_flags & 1) a.ctrl->changed = 1;
         if (s_flags & 2) a.ctrl->status = ST_OVERFLOW;
     }
@@ -231,99 +241,15 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
     if (t0 == 0) {
         Ctrl *c = a.ctrl;
         c->iter = 1;
-        c->in_len = ALGO == CC ? a.n : (style == VERTEX ? 0u : 1u);   // VERTEX: k_scan builds it
+        c->in_len = ALGO == CC ? a.n : (style == VERTEX ? 0u : 1u);   // VERTEX: read from the bitmap
         c->out_len = 0; c->changed = 0; c->cap = cap; c->sel = 0; c->done = 0;
         c->all_active = ALGO == CC ? 1u : 0u;
         c->status = ST_OK; c->source = source;
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
         c->pull = 0; c->found = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
-        c->bar_arrive = 0;
+        c->bar_arrive = 0; c->blk = 0;
         if (ALGO != CC) a.fr0[0] = source;
-    }
-}
-
-// ------------------------------------------------------------------ VERTEX activity scan
-// Topology-driven round, part 1: visit EVERY vertex through
-// its bit in bm[(r-1)%3] and compact the active ones, in vertex order, into
-// the frontier.  Each CTA owns a contiguous range of bitmap words: pass 1
-// counts its set bits (one global atomicAdd per CTA per round), pass 2 writes
-// them warp-cooperatively (one ballot per word: coalesced stores).  Also
-// clears bm[(r+1)%3].
-template <int ALGO, int B>
-__global__ void __launch_bounds__(B) k_scan(Args a) {
-    constexpr int NW = B / 32;
-    Ctrl *c = a.ctrl;
-    if (c->done) return;
-    const uint32_t iter = c->iter, lev = iter - 1;
-    clear_next_bitmap(a, iter);
-    // BFS: levels are written here, in vertex order, for the vertices the
-    // previous round discovered (bm[(r-1)%3]) -- dense sequential stores
-    // instead of one random store per discovery.  A pull round writes the
-    // levels but needs no compacted frontier.
-    const bool compact = !(ALGO == BFS && c->pull);
-    const uint32_t *bm = bm_of(a, iter - 1);
-    __shared__ uint32_t s_w[NW];
-    __shared__ uint32_t s_base;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t per = ((a.nwords + gridDim.x - 1) / gridDim.x + B - 1) / B * B;
-    const uint32_t lo = blockIdx.x * per;
-    const uint32_t hi = lo + per < a.nwords ? lo + per : a.nwords;
-    uint32_t run = 0;
-    if (compact) {   // pass 1: count (block-uniform branch)
-        uint32_t cnt = 0;
-        for (uint32_t i = lo + threadIdx.x; i < hi; i += B) cnt += __popc(bm[i]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-        if (lane == 0) s_w[wid] = cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t t = 0;
-            for (int i = 0; i < NW; i++) t += s_w[i];
-            s_base = t ? atomicAdd(&c->in_len, t) : 0;
-        }
-        __syncthreads();
-        run = s_base;
-        __syncthreads();
-    }
-    // pass 2: write, B words per CTA step, 32 words per warp
-    for (uint32_t i0 = lo; i0 < hi; i0 += B) {   // block-uniform
-        const uint32_t i = i0 + threadIdx.x;
-        const uint32_t w = i < hi ? bm[i] : 0u;
-        if (ALGO == BFS && w) {
-            uint32_t x = w;
-            while (x) {
-                const int bp = __ffs(x) - 1;
-                x &= x - 1;
-                a.val[i * 32u + bp] = (int32_t)lev;
-            }
-        }
-        if (!compact) continue;
-        uint32_t incl = __popc(w);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t excl = incl - __popc(w);
-        if (lane == 31) s_w[wid] = incl;
-        __syncthreads();
-        uint32_t wbase = run, tot = 0;
-        for (int k = 0; k < NW; k++) {
-            const uint32_t x = s_w[k];
-            if (k < wid) wbase += x;
-            tot += x;
-        }
-        __syncthreads();
-        run += tot;
-        const uint32_t wbeg = i0 + 32 * wid;
-        for (int j = 0; j < 32; j++) {   // warp-uniform
-            const uint32_t wj = __shfl_sync(FULL, w, j);
-            if (wj == 0) continue;
-            const uint32_t ej = __shfl_sync(FULL, excl, j);
-            if ((wj >> lane) & 1u)
-                a.fr0[wbase + ej + __popc(wj & ((1u << lane) - 1u))] = (wbeg + j) * 32u + lane;
-        }
     }
 }
 
@@ -410,7 +336,8 @@ template <int B>
 __global__ void __launch_bounds__(B) k_pull(Args a) {
     Ctrl *c = a.ctrl;
     if (c->done || !c->pull) return;
-    const uint32_t iter = c->iter;
+    const uint32_t iter = c->iter, lev = iter - 1;
+    clear_next_bitmap(a, iter);
     const uint32_t *bm_prev = bm_of(a, iter - 1);
     uint32_t *bm_now = bm_of(a, iter);
     const int lane = threadIdx.x & 31;
@@ -420,6 +347,7 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
     for (uint32_t wi = gw; wi < a.nwords; wi += nwarps) {
         const uint32_t visw = a.vis[wi];
         const uint32_t v = wi * 32u + lane;
+        if ((bm_prev[wi] >> lane) & 1u) a.val[v] = (int32_t)lev;   // discovered last round
         bool found = false;
         if (v < a.n && !((visw >> lane) & 1u)) {
             nv++;
@@ -436,25 +364,41 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
         }
         if (found) { nu++; chg = true; }
     }
-    flush_counters<B>(a, nv, ne, nu, chg, false, true);
+    flush_counters<B>(a, nv, ne, nu, chg, false);
 }
 
 // ------------------------------------------------------------------ warp-centric expansion
-// A WARP owns 32 frontier items (or 32 consecutive vertices): a shuffle scan
+// A WARP owns 32 items (frontier entries or active vertices): a shuffle scan
 // turns their out-degrees into offsets and the warp walks the concatenated
 // arc ranges 32*U arcs at a time, each lane finding its item by a 5-step
 // shuffle binary search -- every arc gets one lane whatever the degree
 // distribution (cooperative expansion for skewed RMAT degrees, PAPER.md:
-// 441-446) and consecutive lanes read consecutive col/w words.  There is no
-// block barrier in the loop.  The path is bound by dependent random memory
-// round trips (tools/l2probe.cu), so:
-//  * item loads are software-pipelined two tiles ahead;
-//  * VERTEX relaxations are fire-and-forget: the read filter `cand < val[v]`
-//    decides, atomicMin / the bitmap OR are issued as reductions (RED) whose
-//    results nobody waits for.  A vertex whose read passed the filter is
-//    improved in this round -- by us, or by whoever lowered it further after
-//    our read, who marks it too -- so the marked set is exactly the set of
-//    vertices improved this round (R8);
+// 441-446) and consecutive lanes read consecutive arc words.  There is no
+// block barrier in the loop.
+//
+// Where the items come from:
+//  * sparse rounds (queue styles, small frontier): the frontier queue,
+//    item loads software-pipelined two tiles ahead;
+//  * dense rounds (VERTEX always; queue styles when the frontier exceeds
+//    n / dense_div): the activity bitmap of the previous round, 32 words
+//    (1024 vertices) per warp step, compacted in shared memory -- items come
+//    out in vertex order, so row offsets and arcs are read as ascending
+//    streams instead of one random row per item.
+//
+// Destination blocking (SSSP dense rounds): the value array
+// of a 25M-vertex graph (100 MB) does not stay in L2 next to the streamed
+// arcs, and every gather that misses costs a DRAM sector.  The arcs are
+// therefore stored a second time split by target block (nblk blocks of bsz
+// vertices, bsz*4 bytes sized to stay L2-resident); a dense round walks the
+// frontier once per block, so at any time all warps gather from one block.
+//
+// Relaxations:
+//  * VERTEX: fire-and-forget -- the read filter `cand < val[v]` decides,
+//    atomicMin / the bitmap OR are issued as reductions (RED) whose results
+//    nobody waits for.  A vertex whose read passed the filter is improved in
+//    this round -- by us, or by whoever lowered it further after our read,
+//    who marks it too -- so the marked set is exactly the set of vertices
+//    improved this round (R8);
 //  * queue styles (WORKLIST, DELTA) need the old bitmap word to append each
 //    vertex once; the bitmap bits of the items being expanded are cleared on
 //    the way (every set bit of bm[(r-1)%3] is an item of round r), so the
@@ -477,180 +421,250 @@ __device__ __forceinline__ int32_t ld_value(const int32_t *p, uint64_t pl) {
     return ld_val(p, pl);
 }
 
+constexpr uint32_t NONE = 0xffffffffu;
+
+// Per-round, per-warp expansion state.
+struct Xw {
+    const uint32_t *rows;   // row offsets of the current block (or the plain CSR)
+    const uint2 *arcs;      // (col, w) words (SSSP)
+    uint32_t *bm_now, *bm_prev, *out, *wq;
+    Ctrl *c;
+    uint32_t lev, thr, qn, pend_min;
+    uint64_t pf, pl;
+};
+
+template <int ALGO, bool COHERENT>
+__device__ __forceinline__ void item_rows(const Args &a, const Xw &x, uint32_t u, uint32_t &pay, uint32_t &beg,
+                                          uint32_t &end) {
+    pay = 0; beg = 0; end = 0;
+    if (u != NONE) {
+        if (ALGO != BFS) pay = (uint32_t)ld_value<COHERENT>(a.val + u, x.pl);
+        beg = ld_ro(x.rows + u); end = ld_ro(x.rows + u + 1);
+    }
+}
+
+// Relax the arcs of one 32-item tile (lane: value pay, arcs [beg, beg+deg)).
+template <int ALGO, int STYLE, int U, bool COHERENT>
+__device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, uint32_t deg, uint32_t pay,
+                                           RoundAcc &acc) {
+    constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
+    constexpr int WQ = QUEUE ? 256 : 1;
+    const int lane = threadIdx.x & 31;
+    uint32_t incl = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(FULL, incl, 31);
+    const uint32_t excl = incl - deg;
+    if (lane == 0) acc.ne += total;
+
+    for (uint32_t base = 0; base < total; base += 32 * U) {
+        uint32_t e[U], v[U], p[U];
+        int32_t wt[U], cur[U];
+        bool ok[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const uint32_t k = base + q * 32 + lane;
+            ok[q] = k < total;
+            int j = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t ex = __shfl_sync(FULL, excl, j + st);
+                if (ex <= k) j += st;
+            }
+            const uint32_t bj = __shfl_sync(FULL, beg, j), xj = __shfl_sync(FULL, excl, j);
+            p[q] = __shfl_sync(FULL, pay, j);
+            e[q] = bj + (k - xj);
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            v[q] = 0; wt[q] = 0;
+            if (ok[q]) {
+                if (ALGO == SSSP) {   // one 8-byte (col, w) word
+                    const uint2 w2 = ld_stream2(x.arcs + e[q], x.pf);
+                    v[q] = w2.x; wt[q] = (int32_t)w2.y;
+                } else {
+                    v[q] = ld_stream(a.col + e[q], x.pf);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            cur[q] = 0;
+            if (ok[q]) {
+                if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;
+                else cur[q] = ld_value<COHERENT>(a.val + v[q], x.pl);
+            }
+        }
+        bool need[U];
+        uint32_t citem[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            need[q] = false; citem[q] = 0;
+            if (!ok[q]) continue;
+            if (ALGO == SSSP) {
+                const uint32_t cand = p[q] + (uint32_t)wt[q];
+                if (cand >= (uint32_t)INF) {
+                    acc.ovf = true;
+                } else if ((int32_t)cand < cur[q]) {
+                    atomicMin(a.val + v[q], (int32_t)cand);   // result unused: RED.MIN
+                    acc.nu++; acc.chg = true;
+                    if (STYLE == DELTA && cand >= x.thr) {   // beyond the bucket: park in the far set
+                        atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
+                        x.pend_min = cand < x.pend_min ? cand : x.pend_min;
+                    } else {
+                        need[q] = true; citem[q] = v[q];
+                    }
+                }
+            } else if (ALGO == BFS) {
+                // t.dist > lev+1 -> t.dist = lev+1 (plain store;
+                // concurrent writers store the same value, R9)
+                if (cur[q] == INF) {
+                    if (QUEUE) {   // the queue needs exactly-once: claim
+                        need[q] = true; citem[q] = v[q];
+                    } else {   // the level is written when the vertex is expanded next round
+                        atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
+                        atomicOr(x.bm_now + (v[q] >> 5), 1u << (v[q] & 31));
+                        acc.nu++; acc.chg = true;
+                    }
+                }
+            }
+        }
+        if (STYLE == VERTEX) {
+            if (ALGO == SSSP) {
+#pragma unroll
+                for (int q = 0; q < U; q++)
+                    if (need[q]) atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
+            }
+        } else {
+            uint32_t got[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                got[q] = 0xffffffffu;
+                if (!need[q]) continue;
+                uint32_t *bmp = ALGO == BFS ? a.vis : x.bm_now;
+                got[q] = atomicOr(bmp + (citem[q] >> 5), 1u << (citem[q] & 31));
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
+                if (ALGO == BFS && want) {
+                    a.val[citem[q]] = (int32_t)(x.lev + 1);
+                    atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));   // dense rounds read it
+                    acc.nu++; acc.chg = true;
+                }
+                const unsigned mask = __ballot_sync(FULL, want);
+                if (want) x.wq[x.qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
+                x.qn += __popc(mask);
+            }
+            __syncwarp();
+            if (x.qn > (uint32_t)(WQ > 32 * U ? WQ - 32 * U : 0)) {   // flush the staged appends
+                uint32_t b = 0;
+                if (lane == 0) b = atomicAdd(&x.c->out_len, x.qn);
+                b = __shfl_sync(FULL, b, 0);
+                for (uint32_t i = lane; i < x.qn; i += 32) x.out[b + i] = x.wq[i];
+                __syncwarp();
+                x.qn = 0;
+            }
+        }
+    }
+}
+
+// One round of expansion by this warp.  sit: the warp's 1024-entry shared
+// item list (dense rounds).
 template <int ALGO, int STYLE, int U, bool COHERENT>
 __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, const uint32_t *in,
-                                             uint32_t *out, uint32_t nitems, bool implicit, uint32_t *wq,
-                                             RoundAcc &acc) {
+                                             uint32_t *out, uint32_t nitems, bool dense, bool blocked, uint32_t *wq,
+                                             uint32_t *sit, RoundAcc &acc) {
     constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
-    constexpr int WQ = QUEUE ? 512 : 1;
-    const uint32_t lev = iter - 1;
-    uint32_t *bm_now = bm_of(a, iter);
-    uint32_t *bm_prev = bm_of(a, iter - 1);
-    const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t wstride = nwarps * 32;
-    uint32_t qn = 0;   // warp-uniform count of staged appends
-    uint32_t pend_min = 0xffffffffu;
+    Xw x;
+    x.bm_now = bm_of(a, iter); x.bm_prev = bm_of(a, iter - 1); x.out = out; x.wq = wq; x.c = c;
+    x.lev = iter - 1; x.thr = thr; x.qn = 0; x.pend_min = 0xffffffffu;
+    x.pf = pol_evict_first(); x.pl = pol_evict_last();
+    blocked = blocked && ALGO == SSSP && a.nblk > 1;
+    const uint32_t K = blocked ? a.nblk : 1u;
 
-    auto wflush = [&](uint32_t thresh) {
-        if (qn > thresh) {
-            uint32_t b = 0;
-            if (lane == 0) b = atomicAdd(&c->out_len, qn);
-            b = __shfl_sync(FULL, b, 0);
-            __syncwarp();
-            for (uint32_t i = lane; i < qn; i += 32) out[b + i] = wq[i];
-            __syncwarp();
-            qn = 0;
-        }
-    };
-    auto item_of = [&](uint32_t idx) -> uint32_t {
-        return idx < nitems ? (implicit ? idx : ld_item<COHERENT>(in + idx, pf)) : 0xffffffffu;
-    };
-    // software pipeline: u1 = item of the current tile, u2 = item of the next
-    // tile; pay1/beg1/end1 = value and row offsets of the current tile's item
-    uint32_t wb = gw * 32;
-    uint32_t u1 = item_of(wb + lane), u2 = item_of(wb + wstride + lane);
-    uint32_t pay1 = 0, beg1 = 0, end1 = 0;
-    if (u1 != 0xffffffffu) {
-        if (ALGO != BFS) pay1 = (uint32_t)ld_value<COHERENT>(a.val + u1, pl);
-        beg1 = ld_ro(a.row_off + u1); end1 = ld_ro(a.row_off + u1 + 1);
-    }
-
-    for (; wb < nitems; wb += wstride) {   // warp-uniform
-        const uint32_t u = u1, pay = pay1;
-        uint32_t beg = beg1, deg = end1 - beg1;
-        u1 = u2;
-        u2 = item_of(wb + 2 * wstride + lane);
-        if (u1 != 0xffffffffu) {
-            if (ALGO != BFS) pay1 = (uint32_t)ld_value<COHERENT>(a.val + u1, pl);
-            beg1 = ld_ro(a.row_off + u1); end1 = ld_ro(a.row_off + u1 + 1);
-        } else {
-            pay1 = 0; beg1 = 0; end1 = 0;
-        }
-        if (QUEUE && ALGO != BFS && u != 0xffffffffu) bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
-        if (u == 0xffffffffu || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-        else acc.nv++;
-
-        uint32_t incl = deg;
+    for (uint32_t k = 0; k < K; k++) {
+        const bool first = k == 0, last = k + 1 == K;
+        x.rows = blocked ? a.rowb + (size_t)k * (a.n + 1) : a.row_off;
+        x.arcs = blocked ? a.cwb : a.cw;
+        if (dense) {
+            for (uint32_t g0 = gw * 32; g0 < a.nwords; g0 += wstride) {   // warp-uniform
+                const uint32_t wi = g0 + lane;
+                const uint32_t word = wi < a.nwords ? (COHERENT ? __ldcg(x.bm_prev + wi) : x.bm_prev[wi]) : 0u;
+                const uint32_t cnt = __popc(word);
+                uint32_t incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t total = __shfl_sync(FULL, incl, 31);
-        const uint32_t excl = incl - deg;
-        if (lane == 0) acc.ne += total;
-
-        for (uint32_t base = 0; base < total; base += 32 * U) {
-            uint32_t e[U], v[U], p[U], uj[U];
-            int32_t wt[U], cur[U];
-            bool ok[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                const uint32_t k = base + q * 32 + lane;
-                ok[q] = k < total;
-                int j = 0;
-#pragma unroll
-                for (int st = 16; st > 0; st >>= 1) {
-                    const uint32_t ex = __shfl_sync(FULL, excl, j + st);
-                    if (ex <= k) j += st;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += y;
                 }
-                const uint32_t bj = __shfl_sync(FULL, beg, j), xj = __shfl_sync(FULL, excl, j);
-                p[q] = __shfl_sync(FULL, pay, j);
-                uj[q] = __shfl_sync(FULL, u, j);
-                e[q] = bj + (k - xj);
-            }
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                v[q] = 0; wt[q] = 0;
-                if (ok[q]) {
-                    if (ALGO == SSSP) {   // one 8-byte (col, w) word: one DRAM burst per row
-                        const uint2 x = ld_stream2(a.cw + e[q], pf);
-                        v[q] = x.x; wt[q] = (int32_t)x.y;
-                    } else {
-                        v[q] = ld_stream(a.col + e[q], pf);
+                const uint32_t total = __shfl_sync(FULL, incl, 31);
+                if (total == 0) continue;
+                uint32_t pos = incl - cnt;
+                for (uint32_t y = word; y; y &= y - 1) sit[pos++] = wi * 32u + (uint32_t)(__ffs(y) - 1);
+                if (QUEUE && last && word) x.bm_prev[wi] = 0u;   // recycle the claim bitmap
+                __syncwarp();
+                uint32_t u1 = lane < total ? sit[lane] : NONE, pay1, beg1, end1;
+                item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
+                for (uint32_t j0 = 0; j0 < total; j0 += 32) {   // warp-uniform
+                    const uint32_t u = u1, pay = pay1, beg = beg1;
+                    uint32_t deg = end1 - beg1;
+                    u1 = j0 + 32 + lane < total ? sit[j0 + 32 + lane] : NONE;
+                    item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
+                    if (u != NONE && first) {
+                        acc.nv++;
+                        if (ALGO == BFS && STYLE == VERTEX) a.val[u] = (int32_t)x.lev;   // discovered last round
                     }
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                cur[q] = 0;
-                if (ok[q]) {
-                    if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;
-                    else cur[q] = ld_value<COHERENT>(a.val + v[q], pl);
-                }
-            }
-            bool need[U];
-            uint32_t citem[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                need[q] = false; citem[q] = 0;
-                if (!ok[q]) continue;
-                if (ALGO == SSSP) {
-                    const uint32_t cand = p[q] + (uint32_t)wt[q];
-                    if (cand >= (uint32_t)INF) {
-                        acc.ovf = true;
-                    } else if ((int32_t)cand < cur[q]) {
-                        atomicMin(a.val + v[q], (int32_t)cand);   // result unused: RED.MIN
-                        acc.nu++; acc.chg = true;
-                        if (STYLE == DELTA && cand >= thr) {   // beyond the bucket: park in the far set
-                            atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
-                            pend_min = cand < pend_min ? cand : pend_min;
-                        } else {
-                            need[q] = true; citem[q] = v[q];
-                        }
-                    }
-                } else if (ALGO == BFS) {
-                    // t.dist > lev+1 -> t.dist = lev+1 (plain store;
-                    // concurrent writers store the same value, R9)
-                    if (cur[q] == INF) {
-                        if (QUEUE) {   // the queue needs exactly-once: claim
-                            need[q] = true; citem[q] = v[q];
-                        } else {   // the level is written by the next round's k_scan
-                            atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
-                            atomicOr(bm_now + (v[q] >> 5), 1u << (v[q] & 31));
-                            acc.nu++; acc.chg = true;
-                        }
-                    }
-                }
-            }
-            if (STYLE == VERTEX) {
-                if (ALGO == SSSP) {
-#pragma unroll
-                    for (int q = 0; q < U; q++)
-                        if (need[q]) atomicOr(bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
-                }
-            } else {
-                uint32_t got[U];
-#pragma unroll
-                for (int q = 0; q < U; q++) {
-                    got[q] = 0xffffffffu;
-                    if (!need[q]) continue;
-                    uint32_t *bmp = ALGO == BFS ? a.vis : bm_now;
-                    got[q] = atomicOr(bmp + (citem[q] >> 5), 1u << (citem[q] & 31));
-                }
-#pragma unroll
-                for (int q = 0; q < U; q++) {
-                    const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
-                    if (ALGO == BFS && want) { a.val[citem[q]] = (int32_t)(lev + 1); acc.nu++; acc.chg = true; }
-                    const unsigned mask = __ballot_sync(FULL, want);
-                    if (want) wq[qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
-                    qn += __popc(mask);
+                    if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
+                    relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc);
                 }
                 __syncwarp();
-                wflush(WQ > 32 * U ? WQ - 32 * U : 0);
+            }
+        } else {
+            // software pipeline: u1 = item of the current tile, u2 = item of the next
+            auto item_of = [&](uint32_t idx) -> uint32_t {
+                return idx < nitems ? ld_item<COHERENT>(in + idx, x.pf) : NONE;
+            };
+            uint32_t wb = gw * 32;
+            uint32_t u1 = item_of(wb + lane), u2 = item_of(wb + wstride + lane), pay1, beg1, end1;
+            item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
+            for (; wb < nitems; wb += wstride) {   // warp-uniform
+                const uint32_t u = u1, pay = pay1, beg = beg1;
+                uint32_t deg = end1 - beg1;
+                u1 = u2;
+                u2 = item_of(wb + 2 * wstride + lane);
+                item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
+                if (QUEUE && last && u != NONE) x.bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
+                if (u != NONE && first) acc.nv++;
+                if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
+                relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc);
             }
         }
     }
-    if (QUEUE) { __syncwarp(); wflush(0); }
+    if (QUEUE) {
+        __syncwarp();
+        if (x.qn) {
+            uint32_t b = 0;
+            if (lane == 0) b = atomicAdd(&c->out_len, x.qn);
+            b = __shfl_sync(FULL, b, 0);
+            for (uint32_t i = lane; i < x.qn; i += 32) out[b + i] = wq[i];
+            __syncwarp();
+        }
+    }
     if (STYLE == DELTA) {   // warp-min, one atomicMin per warp
+        uint32_t pm = x.pend_min;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const uint32_t y = __shfl_xor_sync(FULL, pend_min, o);
-            pend_min = y < pend_min ? y : pend_min;
+            const uint32_t y = __shfl_xor_sync(FULL, pm, o);
+            pm = y < pm ? y : pm;
         }
-        if (lane == 0 && pend_min != 0xffffffffu) atomicMin(&c->minpend, pend_min);
+        if (lane == 0 && pm != 0xffffffffu) atomicMin(&c->minpend, pm);
     }
     if (acc.ovf) c->status = ST_OVERFLOW;
 }
@@ -659,17 +673,23 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
 template <int ALGO, int STYLE, int B, int U, int MINB>
 __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     static_assert(STYLE == VERTEX || STYLE == WORKLIST || STYLE == DELTA, "expand is for VERTEX/WORKLIST/DELTA");
-    constexpr int WQ = (STYLE == WORKLIST || STYLE == DELTA) ? 512 : 1;
+    constexpr int WQ = (STYLE == WORKLIST || STYLE == DELTA) ? 256 : 1;
     Ctrl *c = a.ctrl;
     if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull) || (STYLE == DELTA && c->mode != MODE_NEAR)) return;
     const uint32_t iter = c->iter;
+    if (STYLE == VERTEX) clear_next_bitmap(a, iter);
     const uint32_t thr = STYLE == DELTA ? c->thr : 0xffffffffu;
     const uint32_t *in = c->sel ? a.fr1 : a.fr0;
     uint32_t *out = c->sel ? a.fr0 : a.fr1;
+    const uint32_t nitems = c->in_len;
+    const bool dense = STYLE == VERTEX || (a.dense_div && nitems > a.n / a.dense_div);
+    const bool blocked = STYLE == VERTEX ? c->blk != 0 : dense;
     __shared__ uint32_t s_q[B / 32][WQ];
+    __shared__ uint32_t s_it[B / 32][1024];
     RoundAcc acc;
-    expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, c->in_len, false, s_q[threadIdx.x >> 5], acc);
-    flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf, ALGO == BFS && STYLE == VERTEX);
+    expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems, dense, blocked, s_q[threadIdx.x >> 5],
+                                        s_it[threadIdx.x >> 5], acc);
+    flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
 }
 
 // ------------------------------------------------------------------ EDGE style (COO)
@@ -687,7 +707,7 @@ __device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint3
     int32_t ww[4] = {0, 0, 0, 0};
     if (q < m4) {
         if (ALGO == SSSP) {
-            const uint4 x0 = ld_stream4(a.cw + 4ull * q, pf), x1 = ld_stream4(a.cw + 4ull * q + 2, pf);
+            const uint4 x0 = ld_stream4(a.cwb + 4ull * q, pf), x1 = ld_stream4(a.cwb + 4ull * q + 2, pf);
             d[0] = x0.x; ww[0] = (int32_t)x0.y; d[1] = x0.z; ww[1] = (int32_t)x0.w;
             d[2] = x1.x; ww[2] = (int32_t)x1.y; d[3] = x1.z; ww[3] = (int32_t)x1.w;
         } else {
@@ -697,7 +717,7 @@ __device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint3
     } else {
         for (uint32_t j = 0; j < tail; j++) {
             if (ALGO == SSSP) {
-                const uint2 x = ld_stream2(a.cw + 4ull * q + j, pf);
+                const uint2 x = ld_stream2(a.cwb + 4ull * q + j, pf);
                 d[j] = x.x; ww[j] = (int32_t)x.y;
             } else {
                 d[j] = ld_stream(a.col + 4ull * q + j, pf);
@@ -755,6 +775,7 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
     const uint64_t pf = pol_evict_first(), pl = pol_evict_last();
     const uint32_t m4 = a.m >> 2, tail = a.m & 3u;
     const uint32_t nq = m4 + (tail ? 1u : 0u);
+    const uint32_t *srcp = ALGO == SSSP ? a.srcb : a.src;   // SSSP: destination-blocked arc order
     unsigned long long ne = 0, nu = 0;
     bool chg = false, ovf = false;
     const uint32_t stride = gridDim.x * B;
@@ -766,10 +787,10 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
             const uint32_t q = q0 + p * stride;
             s[p][0] = s[p][1] = s[p][2] = s[p][3] = 0;
             if (q < m4) {
-                const uint4 s4 = ld_stream4(a.src + 4ull * q, pf);
+                const uint4 s4 = ld_stream4(srcp + 4ull * q, pf);
                 s[p][0] = s4.x; s[p][1] = s4.y; s[p][2] = s4.z; s[p][3] = s4.w;
             } else if (q < nq) {
-                for (uint32_t j = 0; j < tail; j++) s[p][j] = ld_stream(a.src + 4ull * q + j, pf);
+                for (uint32_t j = 0; j < tail; j++) s[p][j] = ld_stream(srcp + 4ull * q + j, pf);
             }
         }
 #pragma unroll
@@ -808,7 +829,8 @@ __global__ void k_compress(Args a) {
 // (changed == 0) break" / SPEC.md:221 "worklist non-empty"), and drives the
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
-__device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t pull_div) {
+__device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t pull_div,
+                                             uint32_t dense_div) {
     if (c->done) return false;
     c->launches += launches_per_round;
     bool more = STYLE == WORKLIST ? c->out_len > 0 : c->changed != 0;
@@ -839,9 +861,12 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             c->sel ^= 1u;
             c->all_active = 0;
         } else if (STYLE == VERTEX) {
-            c->in_len = 0;   // k_scan rebuilds the frontier of the next round
+            c->in_len = 0;   // VERTEX rounds read the activity bitmap
             // direction-optimising BFS: bottom-up while the next frontier is large
             if (ALGO == BFS) c->pull = pull_div && c->found > n / pull_div;
+            // SSSP: the next round walks the destination-blocked layout when this
+            // round improved many vertices (its frontier is large)
+            c->blk = dense_div && c->found > n / dense_div;
         }
         c->found = 0;
     } else {
@@ -855,9 +880,9 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
 __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
-                          uint32_t n, uint32_t pull_div) {
+                          uint32_t n, uint32_t pull_div, uint32_t dense_div) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div);
+    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, dense_div);
     if (in_graph) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
@@ -875,7 +900,7 @@ __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, u
 __device__ __forceinline__ uint32_t ldv(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
 template <int ALGO, int STYLE>
-__device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32_t pull_div) {
+__device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32_t pull_div, uint32_t dense_div) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const uint32_t gen = ldv(&c->bar_gen);
@@ -883,7 +908,7 @@ __device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32
         const uint32_t arrived = atomicAdd(&c->bar_arrive, 1u);
         if (arrived == gridDim.x - 1) {
             c->bar_arrive = 0;
-            advance_step<ALGO, STYLE>(c, 0u, n, pull_div);
+            advance_step<ALGO, STYLE>(c, 0u, n, pull_div, dense_div);
             __threadfence();
             atomicExch(&c->bar_gen, gen + 1u);
         } else {
@@ -897,7 +922,7 @@ __device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32
 template <int ALGO, int STYLE, int B, int U>
 __global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div, uint32_t max_items) {
     static_assert(STYLE == WORKLIST || STYLE == DELTA, "persistent rounds are for the queue styles");
-    __shared__ uint32_t s_q[B / 32][512];
+    __shared__ uint32_t s_q[B / 32][256];
     Ctrl *c = a.ctrl;
     RoundAcc acc;
     for (;;) {
@@ -913,9 +938,9 @@ __global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div, uin
         if (scan)
             scan_far_round<true>(a, c, iter, thr, out, acc.nv);
         else
-            expand_round<ALGO, STYLE, U, true>(a, c, iter, thr, in, out, ldv(&c->in_len), false,
-                                               s_q[threadIdx.x >> 5], acc);
-        grid_barrier_advance<ALGO, STYLE>(c, a.n, pull_div);
+            expand_round<ALGO, STYLE, U, true>(a, c, iter, thr, in, out, ldv(&c->in_len), false, false,
+                                               s_q[threadIdx.x >> 5], nullptr, acc);
+        grid_barrier_advance<ALGO, STYLE>(c, a.n, pull_div, a.dense_div);
     }
     flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
 }
@@ -1013,6 +1038,42 @@ __global__ void k_rev_scatter(uint64_t m, const uint32_t *src, const uint32_t *c
 __global__ void k_fill_i32(int32_t *p, uint64_t len, int32_t x) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) p[i] = x;
+}
+
+// Destination-blocked layout, built once per graph: block k
+// holds the arcs whose target lies in [k*bsz, (k+1)*bsz), as its own CSR over
+// all sources, rows in source order and arcs in their original order.  One
+// row per thread (rows are short; an RMAT hub row takes one thread µs).
+constexpr uint32_t MAX_BLK = 16;
+__global__ void k_blk_count(uint32_t n, const uint32_t *row_off, const uint32_t *col, uint32_t bsz, uint32_t nblk,
+                            uint32_t *cnt) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint64_t ld = (uint64_t)n + 1;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+        uint32_t c[MAX_BLK];
+        for (uint32_t k = 0; k < nblk; k++) c[k] = 0;
+        const uint32_t e1 = row_off[u + 1];
+        for (uint32_t e = row_off[u]; e < e1; e++) c[col[e] / bsz]++;
+        for (uint32_t k = 0; k < nblk; k++) cnt[k * ld + u] = c[k];
+    }
+    if (blockIdx.x == 0 && threadIdx.x < nblk) cnt[threadIdx.x * ld + n] = 0;
+}
+__global__ void k_blk_scatter(uint32_t n, const uint32_t *row_off, const uint2 *cw, uint32_t bsz, uint32_t nblk,
+                              const uint32_t *rowb, uint2 *cwb, uint32_t *srcb) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint64_t ld = (uint64_t)n + 1;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+        uint32_t pos[MAX_BLK];
+        for (uint32_t k = 0; k < nblk; k++) pos[k] = rowb[k * ld + u];
+        const uint32_t e1 = row_off[u + 1];
+        for (uint32_t e = row_off[u]; e < e1; e++) {
+            const uint2 x = cw[e];
+            const uint32_t k = x.x / bsz;
+            cwb[pos[k]] = x;
+            srcb[pos[k]] = u;
+            pos[k]++;
+        }
+    }
 }
 
 // COO sources in CSR order: src[e] = u for every arc of row u (row-parallel

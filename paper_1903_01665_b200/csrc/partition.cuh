@@ -6,7 +6,7 @@
 // rows of its owned vertices only (global column ids), plus a full-length
 // value array: the owned range is authoritative, the rest holds this part's
 // proposals for remote vertices (the "shadow").  A superstep:
-//   1. relax: the single-GPU VERTEX round (k_scan + k_expand_warp) over the
+//   1. relax: the single-GPU VERTEX round (k_expand_warp) over the
 //      part's rows; MIN lands in the local full-length array;
 //   2. exchange: every owner receives the MIN over all parts of its range
 //      (grouped ncclReduce(ncclMin), one per owner -- volume 4n(P-1)/P per
@@ -278,7 +278,6 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
                 if (algo == CC) {
                     launch_l2(p, k_cc_vertex<BLOCK>, p->grid_cc, s, args[i]);
                 } else {
-                    launch_l2(p, k_scan<SSSP, BLOCK>, p->grid_scan, s, args[i]);
                     launch_expand_warp<SSSP, VERTEX>(p, s, args[i]);
                 }
             }
@@ -324,9 +323,9 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
             }
             for (size_t i = 0; i < g->parts.size(); i++) {
                 if (algo == CC)
-                    k_advance<CC, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u);
+                    k_advance<CC, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u, 0u);
                 else
-                    k_advance<SSSP, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u);
+                    k_advance<SSSP, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u, 0u);
             }
         }
         CU(cudaGetLastError());

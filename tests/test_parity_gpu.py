@@ -106,6 +106,40 @@ def test_parity_delta_stepping(gpu_lib, name, delta):
     assert np.array_equal(out, exp), f"{name}/delta={delta}: {np.flatnonzero(out != exp)[:10]}"
 
 
+# layouts / schedules: (block_bytes, dense_div).  Small blocks force the
+# destination-blocked SSSP layout on reduced graphs (several blocks, a ragged
+# last block); dense_div 1 keeps queue styles sparse except for huge
+# frontiers, 10**6 makes every round dense (bitmap-driven), 0 never dense.
+LAYOUTS = [(4096, 64), (100_000, 10**6), (4 << 20, 1), (0, 64), (32 * 1000 + 4, 0), (65536, 10**6)]
+
+
+@pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s", "ragged", "tiny"])
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("algo", ["sssp", "bfs"])
+def test_parity_layouts(gpu_lib, name, layout, algo):
+    """Every processing style reaches the oracle's fixpoint whatever the
+    destination blocking and the dense/sparse round switch."""
+    G = _graph(name)
+    exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    gpu_lib.falcon_set_option(g, "block_bytes", layout[0])
+    gpu_lib.falcon_set_option(g, "dense_div", layout[1])
+    for style in STYLES + (["delta"] if algo == "sssp" else []):
+        out, st = _run(gpu_lib, g, algo, style, G.source)
+        assert np.array_equal(out, exp), f"{name}/{algo}/{style}/{layout}: {np.flatnonzero(out != exp)[:10]}"
+        out2, _ = _run(gpu_lib, g, algo, style, G.source, device_out=True)   # cached graph, second run
+        assert np.array_equal(out2, exp), f"{name}/{algo}/{style}/{layout} (rerun)"
+
+
+def test_set_option_rejects_unknown(gpu_lib):
+    G = _graph("tiny")
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    with pytest.raises(gpu_lib.FalconError):
+        gpu_lib.falcon_set_option(g, "no_such_option", 1)
+    with pytest.raises(gpu_lib.FalconError):
+        gpu_lib.falcon_set_option(g, "dense_div", -1)
+
+
 def test_delta_rejects_bfs_cc_and_negative(gpu_lib):
     G = _graph("tiny")
     g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
