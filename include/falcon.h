@@ -178,10 +178,13 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
 /* Tuning options of a loaded graph (results never depend on them; they pick
  * the data layout and schedule).  name / value:
  *   "block_bytes"  value-array bytes per destination block of the SSSP arc
- *                  layout (default 24 MiB, env FALCON_BLOCK_MB; 0 = no blocking)
- *   "dense_div"    a round is dense (bitmap-driven, in vertex order; SSSP
- *                  over the blocked layout) when its frontier exceeds
- *                  n / dense_div (default 64, env FALCON_DENSE_DIV; 0 = never)
+ *                  layout (default 64 MiB, env FALCON_BLOCK_MB; 0 = no blocking)
+ *   "dense_div"    a round is dense (bitmap-driven, items in vertex order)
+ *                  when its frontier exceeds n / dense_div (default 16,
+ *                  env FALCON_DENSE_DIV; 0 = never)
+ *   "block_div"    an SSSP round walks the blocked layout when its frontier
+ *                  exceeds n / block_div (default 8, env FALCON_BLOCK_DIV;
+ *                  0 = never)
  *   "pull_div"     BFS VERTEX runs bottom-up while the frontier exceeds
  *                  n / pull_div (default 16; 0 = never)
  *   "persist"      queue styles run small rounds in one cooperative kernel (0/1)

@@ -28,7 +28,8 @@ namespace {
 
 constexpr int BLOCK = 256;
 constexpr int UNROLL = 4;   // arcs per thread per expansion step
-constexpr int EDGE_QP = 4;   // 4-arc quads per thread per step (EDGE style)
+constexpr int EDGE_QP = 4;   // 4-arc quads per lane per chunk (EDGE style)
+constexpr uint32_t ECH = 128u * EDGE_QP;   // arcs per EDGE warp chunk
 constexpr int MINB = 4;     // min resident CTAs per SM for the warp-centric expansion
 constexpr int HOST_CHECK_EVERY = 4;
 
@@ -74,9 +75,11 @@ struct falcon_graph {
     uint2 *cw = nullptr;
     uint32_t *rowb = nullptr, *srcb = nullptr;   // destination-blocked layout (SSSP), built lazily
     uint2 *cwb = nullptr;
+    uint2 *chunk = nullptr, *chunkb = nullptr;   // EDGE chunk source ranges of src / srcb
     uint32_t nblk = 1, bsz = 0;
-    size_t blk_bytes = 24u << 20;        // value-array bytes per block (FALCON_BLOCK_MB)
-    uint32_t dense_div = 64;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV)
+    size_t blk_bytes = 64u << 20;        // value-array bytes per block (FALCON_BLOCK_MB)
+    uint32_t dense_div = 16;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV)
+    uint32_t blk_div = 8;                // blocked round: frontier > n / blk_div (FALCON_BLOCK_DIV)
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     int32_t *val = nullptr;
@@ -120,7 +123,10 @@ struct falcon_graph {
         a.rowb = blk ? rowb : row_off;
         a.cwb = blk ? cwb : a.cw;
         a.srcb = blk ? srcb : src;
+        a.chunk = chunk;
+        a.chunkb = blk ? chunkb : chunk;
         a.dense_div = dense_div;
+        a.blk_div = blk_div;
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
@@ -238,7 +244,7 @@ struct Round {
         launches++;
         launches++;
         k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n, g->pull_div,
-                                                 g->dense_div);
+                                                 g->blk_div);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
     }
@@ -304,7 +310,9 @@ falcon_status_t ensure_src(falcon_graph *g) {
         return FALCON_OK;
     }
     CU(dmalloc(&g->src, (size_t)g->m));
+    CU(dmalloc(&g->chunk, (size_t)((g->m + ECH - 1) / ECH)));
     k_build_src<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->n, (uint32_t)g->m, g->row_off, g->src);
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH, g->src, g->chunk);
     CU(cudaGetLastError());
     return FALCON_OK;
 }
@@ -313,8 +321,13 @@ falcon_status_t ensure_src(falcon_graph *g) {
 // on the device: nblk = ceil(4n / blk_bytes) blocks (1 = not needed).
 falcon_status_t ensure_blocked(falcon_graph *g) {
     if (g->rowb || g->m == 0) return FALCON_OK;
+    {
+        falcon_status_t st = ensure_src(g);   // EDGE chunk ranges of the unblocked order (aliased when nblk == 1)
+        if (st != FALCON_OK) return st;
+    }
     const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
-    uint64_t K = (4 * n + g->blk_bytes - 1) / (g->blk_bytes ? g->blk_bytes : 1);
+    if (g->blk_bytes == 0) return FALCON_OK;
+    uint64_t K = (4 * n + g->blk_bytes - 1) / g->blk_bytes;
     if (K > MAX_BLK) K = MAX_BLK;
     while (K > 1 && K * (n + 1) >= (1ull << 32)) K--;
     if (K <= 1) return FALCON_OK;
@@ -335,6 +348,8 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(g->rowb, len, tiles);
     k_blk_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->cw, bsz, (uint32_t)K, g->rowb, g->cwb,
                                                    g->srcb);
+    CU(dmalloc(&g->chunkb, (size_t)((m + ECH - 1) / ECH)));
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH, g->srcb, g->chunkb);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));
     cudaFree(tiles);
@@ -571,7 +586,7 @@ void destroy(falcon_graph *g) {
     if (g->ev1) cudaEventDestroy(g->ev1);
     cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->cw); cudaFree(g->src);
     cudaFree(g->rin_off); cudaFree(g->rin_col);
-    cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb);
+    cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb); cudaFree(g->chunk); cudaFree(g->chunkb);
     cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1);
     cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
@@ -647,6 +662,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     if (const char *bmb = getenv("FALCON_BLOCK_MB")) g->blk_bytes = (size_t)atoll(bmb) << 20;   // 0: no blocking
     if (const char *dd = getenv("FALCON_DENSE_DIV")) g->dense_div = (uint32_t)atoi(dd);        // 0: never dense
+    if (const char *bd = getenv("FALCON_BLOCK_DIV")) g->blk_div = (uint32_t)atoi(bd);          // 0: never blocked
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_persist;
@@ -826,11 +842,13 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
     for (falcon_graph *t : targets) {
         if (!strcmp(name, "block_bytes")) {
             if (t->stream) cudaStreamSynchronize(t->stream);
-            cudaFree(t->rowb); cudaFree(t->cwb); cudaFree(t->srcb);
-            t->rowb = nullptr; t->cwb = nullptr; t->srcb = nullptr; t->nblk = 1; t->bsz = 0;
+            cudaFree(t->rowb); cudaFree(t->cwb); cudaFree(t->srcb); cudaFree(t->chunkb);
+            t->rowb = nullptr; t->cwb = nullptr; t->srcb = nullptr; t->chunkb = nullptr; t->nblk = 1; t->bsz = 0;
             t->blk_bytes = (size_t)value;
         } else if (!strcmp(name, "dense_div")) {
             t->dense_div = (uint32_t)value;
+        } else if (!strcmp(name, "block_div")) {
+            t->blk_div = (uint32_t)value;
         } else if (!strcmp(name, "pull_div")) {
             t->pull_div = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {

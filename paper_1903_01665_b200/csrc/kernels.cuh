@@ -79,8 +79,11 @@ struct Args {
     const uint32_t *rowb;      // [nblk*(n+1)]
     const uint2 *cwb;          // [m]
     const uint32_t *srcb;      // [m] EDGE style
+    const uint2 *chunk;        // [m/ECH] source range [min, max] of each EDGE chunk of src (CSR order)
+    const uint2 *chunkb;       // ... of srcb (blocked order)
     uint32_t nblk;
     uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
+    uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
@@ -437,9 +440,9 @@ template <int ALGO, bool COHERENT>
 __device__ __forceinline__ void item_rows(const Args &a, const Xw &x, uint32_t u, uint32_t &pay, uint32_t &beg,
                                           uint32_t &end) {
     pay = 0; beg = 0; end = 0;
-    if (u != NONE) {
-        if (ALGO != BFS) pay = (uint32_t)ld_value<COHERENT>(a.val + u, x.pl);
-        beg = ld_ro(x.rows + u); end = ld_ro(x.rows + u + 1);
+    if (u != NONE) {   // the item's own value and offsets: streamed, evict-first (keep L2 for the gathers)
+        if (ALGO != BFS) pay = (uint32_t)ld_value<COHERENT>(a.val + u, x.pf);
+        beg = ld_stream(x.rows + u, x.pf); end = ld_stream(x.rows + u + 1, x.pf);
     }
 }
 
@@ -594,9 +597,14 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
         x.rows = blocked ? a.rowb + (size_t)k * (a.n + 1) : a.row_off;
         x.arcs = blocked ? a.cwb : a.cw;
         if (dense) {
+            auto word_at = [&](uint32_t wi) -> uint32_t {
+                return wi < a.nwords ? (COHERENT ? __ldcg(x.bm_prev + wi) : x.bm_prev[wi]) : 0u;
+            };
+            uint32_t wnext = word_at(gw * 32 + lane);   // next group's word, one group ahead
             for (uint32_t g0 = gw * 32; g0 < a.nwords; g0 += wstride) {   // warp-uniform
                 const uint32_t wi = g0 + lane;
-                const uint32_t word = wi < a.nwords ? (COHERENT ? __ldcg(x.bm_prev + wi) : x.bm_prev[wi]) : 0u;
+                const uint32_t word = wnext;
+                wnext = word_at(g0 + wstride + lane);
                 const uint32_t cnt = __popc(word);
                 uint32_t incl = cnt;
 #pragma unroll
@@ -683,7 +691,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     uint32_t *out = c->sel ? a.fr0 : a.fr1;
     const uint32_t nitems = c->in_len;
     const bool dense = STYLE == VERTEX || (a.dense_div && nitems > a.n / a.dense_div);
-    const bool blocked = STYLE == VERTEX ? c->blk != 0 : dense;
+    const bool blocked = STYLE == VERTEX ? c->blk != 0 : (a.blk_div && nitems > a.n / a.blk_div);
     __shared__ uint32_t s_q[B / 32][WQ];
     __shared__ uint32_t s_it[B / 32][1024];
     RoundAcc acc;
@@ -693,11 +701,9 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
 }
 
 // ------------------------------------------------------------------ EDGE style (COO)
-// QP quads of four CSR-ordered arcs per thread per step: all QP 16-byte src
-// loads are issued first and the sources' activity bits (bm[(r-1)%3],
-// L1/L2-resident) tested, so a mostly-inactive round streams src[] with QP
-// loads in flight per thread; col/w are fetched only for quads with an
-// active source.
+// Per quad of four consecutive arcs whose sources' activity bits
+// (bm[(r-1)%3], L1/L2-resident) are in actmask: col/w are fetched only for
+// quads with an active source.
 template <int ALGO>
 __device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint32_t (&s)[4], uint32_t actmask,
                                           uint32_t m4, uint32_t tail, uint32_t lev, uint32_t *bm_now, uint64_t pf,
@@ -753,19 +759,21 @@ __device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint3
                 atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
                 nu++; chg = true;
             }
-        } else {
-            const uint32_t lu = pay[j], lv = (uint32_t)cur[j];
-            if (lu != lv) {
-                const uint32_t hi = lu > lv ? lu : lv, lo = lu > lv ? lv : lu;
-                atomicMin(a.val + hi, (int32_t)lo);
-                nu++; chg = true;
-            }
         }
     }
 }
 
+// A warp owns a chunk of ECH = 128*QP consecutive arcs (lane: QP quads, 16-byte
+// loads, consecutive lanes on consecutive quads).  The chunk's source range
+// [lo, hi] is precomputed at load time (k_chunk_range); when the activity
+// bitmap shows no active source in it, the warp skips the chunk without
+// reading src[] -- a sparse round streams 4 bytes of bitmap per 32 sources
+// instead of 4 bytes of src[] per arc.  In a dense round every arc's source
+// bit is tested.
 template <int ALGO, int B, int QP>
 __global__ void __launch_bounds__(B) k_edge(Args a) {
+    static_assert(ALGO != CC, "CC has its own EDGE kernel (cc.cuh)");
+    constexpr uint32_t ECH = 128u * QP;
     Ctrl *c = a.ctrl;
     if (c->done) return;
     const uint32_t iter = c->iter, lev = iter - 1;
@@ -776,37 +784,71 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
     const uint32_t m4 = a.m >> 2, tail = a.m & 3u;
     const uint32_t nq = m4 + (tail ? 1u : 0u);
     const uint32_t *srcp = ALGO == SSSP ? a.srcb : a.src;   // SSSP: destination-blocked arc order
+    const uint2 *rng = ALGO == SSSP ? a.chunkb : a.chunk;
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
+    const uint32_t nch = (a.m + ECH - 1) / ECH;
     unsigned long long ne = 0, nu = 0;
     bool chg = false, ovf = false;
-    const uint32_t stride = gridDim.x * B;
-    for (uint32_t q0 = blockIdx.x * B + threadIdx.x; q0 < nq; q0 += stride * QP) {
-        uint32_t s[QP][4];
+    for (uint32_t ch = gw; ch < nch; ch += nwarps) {   // warp-uniform
+        const uint2 r = rng[ch];
+        const uint32_t w0 = r.x >> 5, nw = (r.y >> 5) - w0 + 1;
+        if (nw <= 32) {   // one bitmap word per lane: skip the chunk if no source is active
+            const uint32_t word = (uint32_t)lane < nw ? bm_prev[w0 + lane] : 0u;
+            if (!__any_sync(FULL, word != 0u)) continue;
+        }
+        uint32_t sq[QP][4];
         uint32_t act[QP];
 #pragma unroll
         for (int p = 0; p < QP; p++) {
-            const uint32_t q = q0 + p * stride;
-            s[p][0] = s[p][1] = s[p][2] = s[p][3] = 0;
+            const uint32_t q = ch * (ECH / 4) + p * 32 + lane;
+            sq[p][0] = sq[p][1] = sq[p][2] = sq[p][3] = 0;
             if (q < m4) {
                 const uint4 s4 = ld_stream4(srcp + 4ull * q, pf);
-                s[p][0] = s4.x; s[p][1] = s4.y; s[p][2] = s4.z; s[p][3] = s4.w;
+                sq[p][0] = s4.x; sq[p][1] = s4.y; sq[p][2] = s4.z; sq[p][3] = s4.w;
             } else if (q < nq) {
-                for (uint32_t j = 0; j < tail; j++) s[p][j] = ld_stream(srcp + 4ull * q + j, pf);
+                for (uint32_t j = 0; j < tail; j++) sq[p][j] = ld_stream(srcp + 4ull * q + j, pf);
             }
         }
 #pragma unroll
         for (int p = 0; p < QP; p++) {
-            const uint32_t q = q0 + p * stride;
+            const uint32_t q = ch * (ECH / 4) + p * 32 + lane;
             const uint32_t cntq = q < m4 ? 4u : (q < nq ? tail : 0u);
             act[p] = 0;
 #pragma unroll
-            for (int j = 0; j < 4; j++)   // ALGO == CC: every arc hooks; otherwise the source must be active
-                if ((uint32_t)j < cntq && (ALGO == CC || bit_test(bm_prev, s[p][j]))) act[p] |= 1u << j;
+            for (int j = 0; j < 4; j++)   // the source must be active (improved / discovered last round)
+                if ((uint32_t)j < cntq && bit_test(bm_prev, sq[p][j])) act[p] |= 1u << j;
         }
 #pragma unroll
         for (int p = 0; p < QP; p++)
-            if (act[p]) edge_quad<ALGO>(a, q0 + p * stride, s[p], act[p], m4, tail, lev, bm_now, pf, pl, ne, nu, chg, ovf);
+            if (act[p])
+                edge_quad<ALGO>(a, ch * (ECH / 4) + p * 32 + lane, sq[p], act[p], m4, tail, lev, bm_now, pf, pl, ne,
+                                nu, chg, ovf);
     }
     flush_counters<B>(a, 0ull, ne, nu, chg, ovf);
+}
+
+// Source range [min, max] of every ECH-arc chunk of a COO source array (one
+// warp per chunk; load time).
+__global__ void k_chunk_range(uint32_t m, uint32_t ech, const uint32_t *src, uint2 *rng) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nch = (m + ech - 1) / ech;
+    for (uint32_t ch = gw; ch < nch; ch += nwarps) {
+        uint32_t lo = 0xffffffffu, hi = 0;
+        const uint32_t e1 = (ch + 1) * ech < m ? (ch + 1) * ech : m;
+        for (uint32_t e = ch * ech + lane; e < e1; e += 32) {
+            const uint32_t u = src[e];
+            lo = u < lo ? u : lo;
+            hi = u > hi ? u : hi;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+            hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+        }
+        if (lane == 0) rng[ch] = make_uint2(lo, hi);
+    }
 }
 
 // ------------------------------------------------------------------ CC pointer jumping
@@ -830,7 +872,7 @@ __global__ void k_compress(Args a) {
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
 __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t pull_div,
-                                             uint32_t dense_div) {
+                                             uint32_t blk_div) {
     if (c->done) return false;
     c->launches += launches_per_round;
     bool more = STYLE == WORKLIST ? c->out_len > 0 : c->changed != 0;
@@ -866,7 +908,7 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             if (ALGO == BFS) c->pull = pull_div && c->found > n / pull_div;
             // SSSP: the next round walks the destination-blocked layout when this
             // round improved many vertices (its frontier is large)
-            c->blk = dense_div && c->found > n / dense_div;
+            c->blk = blk_div && c->found > n / blk_div;
         }
         c->found = 0;
     } else {
@@ -880,9 +922,9 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
 __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
-                          uint32_t n, uint32_t pull_div, uint32_t dense_div) {
+                          uint32_t n, uint32_t pull_div, uint32_t blk_div) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, dense_div);
+    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div);
     if (in_graph) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
@@ -900,7 +942,7 @@ __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, u
 __device__ __forceinline__ uint32_t ldv(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
 template <int ALGO, int STYLE>
-__device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32_t pull_div, uint32_t dense_div) {
+__device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32_t pull_div, uint32_t blk_div) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const uint32_t gen = ldv(&c->bar_gen);
@@ -908,7 +950,7 @@ __device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32
         const uint32_t arrived = atomicAdd(&c->bar_arrive, 1u);
         if (arrived == gridDim.x - 1) {
             c->bar_arrive = 0;
-            advance_step<ALGO, STYLE>(c, 0u, n, pull_div, dense_div);
+            advance_step<ALGO, STYLE>(c, 0u, n, pull_div, blk_div);
             __threadfence();
             atomicExch(&c->bar_gen, gen + 1u);
         } else {
@@ -940,7 +982,7 @@ __global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div, uin
         else
             expand_round<ALGO, STYLE, U, true>(a, c, iter, thr, in, out, ldv(&c->in_len), false, false,
                                                s_q[threadIdx.x >> 5], nullptr, acc);
-        grid_barrier_advance<ALGO, STYLE>(c, a.n, pull_div, a.dense_div);
+        grid_barrier_advance<ALGO, STYLE>(c, a.n, pull_div, a.blk_div);
     }
     flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
 }

@@ -106,11 +106,13 @@ def test_parity_delta_stepping(gpu_lib, name, delta):
     assert np.array_equal(out, exp), f"{name}/delta={delta}: {np.flatnonzero(out != exp)[:10]}"
 
 
-# layouts / schedules: (block_bytes, dense_div).  Small blocks force the
-# destination-blocked SSSP layout on reduced graphs (several blocks, a ragged
-# last block); dense_div 1 keeps queue styles sparse except for huge
-# frontiers, 10**6 makes every round dense (bitmap-driven), 0 never dense.
-LAYOUTS = [(4096, 64), (100_000, 10**6), (4 << 20, 1), (0, 64), (32 * 1000 + 4, 0), (65536, 10**6)]
+# layouts / schedules: (block_bytes, dense_div, block_div).  Small blocks
+# force the destination-blocked SSSP layout on reduced graphs (several blocks,
+# a ragged last block); dense_div 1 keeps queue styles sparse except for huge
+# frontiers, 10**6 makes every round dense (bitmap-driven), 0 never dense;
+# block_div 10**6 walks the blocked layout in every dense round, 0 never.
+LAYOUTS = [(4096, 64, 10**6), (100_000, 10**6, 10**6), (4 << 20, 1, 8), (0, 64, 8), (32 * 1000 + 4, 0, 10**6),
+           (65536, 10**6, 0), (65536, 64, 8)]
 
 
 @pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s", "ragged", "tiny"])
@@ -124,6 +126,7 @@ def test_parity_layouts(gpu_lib, name, layout, algo):
     g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
     gpu_lib.falcon_set_option(g, "block_bytes", layout[0])
     gpu_lib.falcon_set_option(g, "dense_div", layout[1])
+    gpu_lib.falcon_set_option(g, "block_div", layout[2])
     for style in STYLES + (["delta"] if algo == "sssp" else []):
         out, st = _run(gpu_lib, g, algo, style, G.source)
         assert np.array_equal(out, exp), f"{name}/{algo}/{style}/{layout}: {np.flatnonzero(out != exp)[:10]}"
