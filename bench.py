@@ -78,19 +78,20 @@ def m_counted(G, algo, out) -> int:
 
 
 def algorithmic_bytes(algo, style, st, n, m) -> int:
-    """Bytes the relax kernel must move for the work it did:
-    per processed vertex 8 (row_off amortised 4 + own value 4) [+4 frontier
-    read, WORKLIST]; per relaxed arc 12 (SSSP: col, w, gathered value) or 8
-    (BFS/CC: col, gathered value); per successful update 4 [+4 append];
-    VERTEX scans one activity word per vertex per round; EDGE streams src[]
-    (4 B per arc per round) and gathers the source value (4 B per active arc)."""
+    """Bytes the relax kernels must move for the work they did (SURVEY.md
+    §8(d) units): per relaxed arc 12 (SSSP: col, w, gathered
+    target value) or 8 (BFS: col, target's visited word); per successful
+    update 4 (the atomic write).  Per processed item: VERTEX 8 (row offset,
+    own value); queue styles 12 (+ the frontier entry) and 4 per append.
+    VERTEX and EDGE read the activity bitmap (n/8 bytes) every round; EDGE
+    adds per relaxed arc the 4-byte source id and the 4-byte source value."""
     per_arc = 12 if algo == "sssp" else 8
     V, E, U, R = st["vertices_processed"], st["edges_relaxed"], st["updates"], st["iterations"]
     b = E * per_arc + U * 4
     if style == "vertex":
-        b += V * 8 + R * 4 * n
+        b += V * 8 + R * n // 8
     elif style == "edge":
-        b += R * 4 * m + E * 4
+        b += E * 8 + R * n // 8
     else:
         b += V * 12 + U * 4
     return int(b)
@@ -114,6 +115,10 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()   # the timed region starts once the sampler is producing rows
+            while not self.rows and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.02)
+            self.n0 = len(self.rows)
         except Exception:
             self.proc = None
         return self
@@ -124,6 +129,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            t0 = time.time()   # at least two samples taken while the timed region ran
+            while len(self.rows) < self.n0 + 2 and time.time() - t0 < 2 and self.proc.poll() is None:
+                time.sleep(0.02)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)

@@ -30,7 +30,6 @@ constexpr int BLOCK = 256;
 constexpr int UNROLL = 4;   // arcs per thread per expansion step
 constexpr int EDGE_QP = 4;   // 4-arc quads per lane per chunk (EDGE style)
 constexpr uint32_t ECH = 128u * EDGE_QP;   // arcs per EDGE warp chunk
-constexpr int MINB = 4;     // min resident CTAs per SM for the warp-centric expansion
 constexpr int HOST_CHECK_EVERY = 4;
 
 thread_local std::string g_last_error;
@@ -84,13 +83,14 @@ struct falcon_graph {
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     int32_t *val = nullptr;
     uint32_t *bm = nullptr, *fr0 = nullptr, *fr1 = nullptr;   // bm: 4 bitmaps of nwords
+    uint32_t *tiles = nullptr;           // scan tile sums (load-time layout builds)
     uint32_t nwords = 0;
     Ctrl *ctrl = nullptr;
     Ctrl *h_ctrl = nullptr;
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_persist = 0, grid_expand_fr = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    int grid_persist = 0, grid_expand_fr = 0, grid_expand_dl = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
     cudaGraph_t graphs[3][4] = {};
     cudaGraphExec_t execs[3][4] = {};
     int32_t delta = 0;                   // DELTA bucket width (0 = auto: max(1, average weight))
@@ -195,11 +195,14 @@ cudaError_t launch_coop(const falcon_graph *g, void (*k)(KArgs...), int grid, cu
 template <int ALGO, int STYLE>
 void launch_expand_warp(const falcon_graph *g, cudaStream_t s, const Args &a) {
     switch (g->variant) {
-    case 1: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 8>, g->grid_expand_fr, s, a); break;
-    case 2: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 2>, g->grid_expand_fr, s, a); break;
-    case 3: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 3>, g->grid_expand_fr, s, a); break;
-    case 4: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 6>, g->grid_expand_fr, s, a); break;
-    default: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, UNROLL, MINB>, g->grid_expand_fr, s, a); break;
+    case 1: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 4>, g->grid_expand_fr, s, a); break;
+    case 2: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 3>, g->grid_expand_fr, s, a); break;
+    case 3: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 6>, g->grid_expand_fr, s, a); break;
+    case 4: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 2>, g->grid_expand_fr, s, a); break;
+    default:   // tuned per style (tools/survey.py sweeps on rand-25M / rmat-10M)
+        if (STYLE == DELTA) launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 4>, g->grid_expand_dl, s, a);
+        else launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 3>, g->grid_expand_fr, s, a);
+        break;
     }
 }
 
@@ -337,11 +340,10 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     cudaStream_t s = g->stream;
     const uint64_t len = K * (n + 1);
     const uint32_t ntiles = (uint32_t)((len + 1023) / 1024);
-    uint32_t *tiles = nullptr;
+    uint32_t *tiles = g->tiles;
     CU(dmalloc(&g->rowb, len));
     CU(dmalloc(&g->cwb, m));
     CU(dmalloc(&g->srcb, m));
-    CU(dmalloc(&tiles, ntiles));
     k_blk_count<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->col, bsz, (uint32_t)K, g->rowb);
     k_scan_local<<<ntiles, 256, 0, s>>>(g->rowb, len, tiles);
     k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
@@ -352,7 +354,6 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH, g->srcb, g->chunkb);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));
-    cudaFree(tiles);
     g->nblk = (uint32_t)K;
     g->bsz = bsz;
     return FALCON_OK;
@@ -365,10 +366,8 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
     cudaStream_t s = g->stream;
     CU(dmalloc(&g->rin_off, n + 1));
     CU(dmalloc(&g->rin_col, m));
-    uint32_t *cursor = nullptr, *tiles = nullptr;
+    uint32_t *cursor = g->fr1, *tiles = g->tiles;   // load-time scratch (no run is in flight)
     const uint32_t ntiles = (uint32_t)((n + 1 + 1023) / 1024);
-    CU(dmalloc(&cursor, n + 1));
-    CU(dmalloc(&tiles, ntiles));
     CU(cudaMemsetAsync(g->rin_off, 0, (n + 1) * 4, s));
     if (m) k_indeg<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->col, g->rin_off);
     k_scan_local<<<ntiles, 256, 0, s>>>(g->rin_off, n + 1, tiles);
@@ -378,12 +377,13 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
     if (m) {
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
-        k_rev_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->src, g->col, cursor, g->rin_col);
+        const uint64_t win = 8u << 20;   // targets per pass: 32 MB of cursors
+        for (uint64_t lo = 0; lo < n; lo += win)
+            k_rev_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->src, g->col, cursor, g->rin_col, (uint32_t)lo,
+                                                           (uint32_t)(lo + win < n ? lo + win : n));
     }
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));
-    cudaFree(cursor);
-    cudaFree(tiles);
     return FALCON_OK;
 }
 
@@ -587,7 +587,7 @@ void destroy(falcon_graph *g) {
     cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->cw); cudaFree(g->src);
     cudaFree(g->rin_off); cudaFree(g->rin_col);
     cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb); cudaFree(g->chunk); cudaFree(g->chunkb);
-    cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1);
+    cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1); cudaFree(g->tiles);
     cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -620,8 +620,9 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     CU(dmalloc(&g->val, (size_t)n));
     g->nwords = (uint32_t)((((n + 31) / 32) + 3) & ~3ll);
     CU(dmalloc(&g->bm, 4 * (size_t)g->nwords));
-    CU(dmalloc(&g->fr0, (size_t)n));
-    CU(dmalloc(&g->fr1, (size_t)n));
+    CU(dmalloc(&g->fr0, (size_t)n + 1));
+    CU(dmalloc(&g->fr1, (size_t)n + 1));   // n+1: doubles as the reverse-CSR cursor at build time
+    CU(dmalloc(&g->tiles, (size_t)(MAX_BLK * ((uint64_t)n + 1) + 1023) / 1024 + 1));   // scan tile sums
     CU(dmalloc(&g->ctrl, 1));
     CU(dmalloc(&g->d_flags, 1));
     CU(cudaMallocHost(&g->h_ctrl, sizeof(Ctrl)));
@@ -637,7 +638,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     int occ_f = 0, occ_e = 0, occ_p = 0;
     const char *var = getenv("FALCON_EXPAND_VARIANT");
     g->variant = var ? atoi(var) : 0;
-    static const int var_minb[5] = {MINB, 8, 2, 3, 6};
+    static const int var_minb[5] = {3, 4, 3, 6, 2};
     occ_f = var_minb[g->variant >= 0 && g->variant < 5 ? g->variant : 0];
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_persist<SSSP, DELTA, BLOCK, UNROLL>, BLOCK, 0));
     {
@@ -656,6 +657,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     auto full = [&](int occ) { return (int64_t)g->num_sms * (occ > 0 ? occ : 1); };
     g->grid_persist = (int)full(occ_p);
     g->grid_expand_fr = clampg((n + BLOCK - 1) / BLOCK, full(occ_f));
+    g->grid_expand_dl = clampg((n + BLOCK - 1) / BLOCK, full(g->variant ? occ_f : 4));
     g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP - 1) / (BLOCK * EDGE_QP), full(occ_e));
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     g->grid_cc = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
@@ -666,7 +668,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_persist;
-    for (int gsz : {g->grid_expand_fr, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull})
+    for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull})
         if (gsz > slots) slots = gsz;
     g->cnt_slots = slots;
     CU(dmalloc(&g->cnt, 3 * (size_t)slots));

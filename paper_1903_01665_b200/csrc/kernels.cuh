@@ -463,10 +463,11 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
     const uint32_t excl = incl - deg;
     if (lane == 0) acc.ne += total;
 
-    for (uint32_t base = 0; base < total; base += 32 * U) {
-        uint32_t e[U], v[U], p[U];
-        int32_t wt[U], cur[U];
-        bool ok[U];
+    // Two-stage software pipeline over steps of 32*U arcs: the (col, w) loads
+    // of step i+1 are issued before the value gathers of step i are consumed,
+    // so each lane keeps 2U independent loads in flight.
+    auto stage1 = [&](uint32_t base, uint32_t (&v)[U], int32_t (&wt)[U], uint32_t (&p)[U], bool (&ok)[U]) {
+        uint32_t e[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
             const uint32_t k = base + q * 32 + lane;
@@ -493,6 +494,13 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
                 }
             }
         }
+    };
+    uint32_t v[U], p[U];
+    int32_t wt[U];
+    bool ok[U];
+    if (total) stage1(0, v, wt, p, ok);
+    for (uint32_t base = 0; base < total; base += 32 * U) {   // warp-uniform
+        int32_t cur[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
             cur[q] = 0;
@@ -501,6 +509,11 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
                 else cur[q] = ld_value<COHERENT>(a.val + v[q], x.pl);
             }
         }
+        uint32_t vn[U], pn[U];
+        int32_t wtn[U];
+        bool okn[U];
+        const bool more = base + 32 * U < total;
+        if (more) stage1(base + 32 * U, vn, wtn, pn, okn);
         bool need[U];
         uint32_t citem[U];
 #pragma unroll
@@ -571,6 +584,10 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
                 __syncwarp();
                 x.qn = 0;
             }
+        }
+        if (more) {
+#pragma unroll
+            for (int q = 0; q < U; q++) { v[q] = vn[q]; wt[q] = wtn[q]; p[q] = pn[q]; ok[q] = okn[q]; }
         }
     }
 }
@@ -1069,12 +1086,27 @@ __global__ void k_scan_add(uint32_t *x, uint64_t len, const uint32_t *tile_sums)
     if (i < len) x[i] += tile_sums[i / 1024];
 }
 // arc-parallel scatter of the COO arcs into the in-rows (in-row order is
-// arbitrary: BFS levels and CC labels do not depend on it)
+// arbitrary: BFS levels and CC labels do not depend on it).  One pass per
+// window of targets [lo, hi): the window's cursors (<= 32 MB) stay
+// L2-resident, so the position atomics run at L2 rate instead of missing to
+// DRAM; col[] is streamed once per window (evict-first).
 __global__ void k_rev_scatter(uint64_t m, const uint32_t *src, const uint32_t *col, uint32_t *cursor,
-                              uint32_t *rin_col) {
+                              uint32_t *rin_col, uint32_t lo, uint32_t hi) {
+    const uint64_t pf = pol_evict_first();
+    const uint64_t m4 = m >> 2;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride)
-        rin_col[atomicAdd(cursor + col[e], 1u)] = src[e];
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= m4; q += stride) {
+        uint32_t c[4] = {hi, hi, hi, hi};
+        if (q < m4) {
+            const uint4 c4 = ld_stream4(col + 4 * q, pf);
+            c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+        } else {
+            for (uint64_t j = 0; 4 * q + j < m; j++) c[j] = col[4 * q + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (c[j] >= lo && c[j] < hi) rin_col[atomicAdd(cursor + c[j], 1u)] = ld_stream(src + 4 * q + j, pf);
+    }
 }
 
 __global__ void k_fill_i32(int32_t *p, uint64_t len, int32_t x) {

@@ -20,4 +20,5 @@ for rep in range(2):
         for s in ("vertex", "edge", "worklist"):
             t = time.perf_counter(); st = fb.run(g, a, s, out, G.source); t1 = time.perf_counter()
             print(f"   first {a}/{s}: wall {1e3*(t1-t):.2f} ms  device {st.ms:.2f} ms")
-    fb.graph_free(g)
+    t = time.perf_counter(); fb.graph_free(g); torch.cuda.synchronize()
+    print(f"   free: {1e3*(time.perf_counter()-t):.1f} ms")
