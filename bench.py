@@ -97,6 +97,18 @@ def algorithmic_bytes(algo, style, st, n, m) -> int:
     return int(b)
 
 
+def l2_ops(algo, style, st):
+    """L2 operations (in random-gather slots) the relax kernels issue for the
+    work they did: one gather per relaxed arc, per successful SSSP update one
+    RED.MIN (~4 slots) and one activity-bitmap OR (~1.1 slots), per BFS
+    discovery two bitmap ORs (profiles/l2_peaks.json)."""
+    pk = json.load(open(os.path.join(ROOT, "profiles", "l2_peaks.json")))
+    E, U = st["edges_relaxed"], st["updates"]
+    if algo == "sssp":
+        return E + U * (pk["red_min_cost_in_gathers"] + pk["red_or_bitmap_cost_in_gathers"])
+    return E + U * 2 * pk["red_or_bitmap_cost_in_gathers"]
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -332,6 +344,16 @@ def main():
                     "traffic": ncu_traffic(key), "kernel": f"relax {key}", "peak_source": hbm_src,
                     "relax_ms": dst["relax_ms"], "relax_launches": dst["relax_launches"],
                     "algorithmic_bytes": bytes_dom, "share_of_step": dst["relax_ms"] / ms_step}
+        # secondary ceiling: random L2 operations (the path's real bound)
+        try:
+            pk = json.load(open(os.path.join(ROOT, "profiles", "l2_peaks.json")))
+            ops = l2_ops(dom[0], dom[1], dst)
+            ach = ops / (dst["relax_ms"] * 1e-3) / 1e9
+            roofline["l2_ops"] = {"achieved": ach, "peak": pk["gather_gops_window_le_64MB"], "unit": "G gather-slots/s",
+                                  "frac": ach / pk["gather_gops_window_le_64MB"], "ops": ops,
+                                  "peak_source": "profiles/l2_peaks.json (tools/l2probe3.cu)"}
+        except (OSError, KeyError, ValueError):
+            pass
     else:   # partitioned: the whole superstep loop (relax + exchange) of the slowest algorithm
         worst = max(per_run, key=lambda k: statistics.median(x["ms"] for x in per_run[k]))
         x = per_run[worst][-1]

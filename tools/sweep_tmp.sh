@@ -1,4 +1,4 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
-python tools/survey.py --configs rand-25M,rmat-10M,grid-24M --reps 3 > gpurun_out/survey.log 2>&1
-python tools/e2e_timing.py > gpurun_out/e2e_timing.log 2>&1
-timeout 600 python bench.py --out gpurun_out/bench.json > gpurun_out/bench.log 2>&1
+for D in 25 50 100 200 400 1000; do
+for C in rand-25M rmat-10M; do
+python tools/run_one.py --config $C --algo sssp --style delta --reps 3 --delta $D 2>&1 | grep "rep2" | sed "s/^/$C delta=$D /"
+done; done
