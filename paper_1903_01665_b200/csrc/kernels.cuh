@@ -29,6 +29,9 @@
 namespace fk {
 
 constexpr int32_t INF = 0x7fffffff;   // MAX_INT
+#ifdef FK_PROBE
+__device__ int fk_probe_mode;   // tools/expand_probe.cu only (never defined in the product build)
+#endif
 constexpr unsigned FULL = 0xffffffffu;
 
 enum Algo : int { SSSP = 0, BFS = 1, CC = 2 };
@@ -446,12 +449,126 @@ __device__ __forceinline__ void item_rows(const Args &a, const Xw &x, uint32_t u
     }
 }
 
-// Relax the arcs of one 32-item tile (lane: value pay, arcs [beg, beg+deg)).
+// One step of 32*U arcs whose (col, w) loads have been issued; relaxed one
+// step later (cross-tile software pipeline, see relax_tile).
+template <int U>
+struct Step {
+    uint32_t v[U], p[U];
+    int32_t wt[U];
+    bool ok[U];
+    bool live;
+};
+
+// Gather the targets' values of a loaded step and relax its arcs.
 template <int ALGO, int STYLE, int U, bool COHERENT>
-__device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, uint32_t deg, uint32_t pay,
-                                           RoundAcc &acc) {
+__device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &s, RoundAcc &acc) {
     constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
     constexpr int WQ = QUEUE ? 256 : 1;
+    const int lane = threadIdx.x & 31;
+#ifdef FK_PROBE   // tools/expand_probe.cu: time the expansion without (0) / with (1) the gathers
+    if (fk_probe_mode < 2) {
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            if (!s.ok[q]) continue;
+            const int32_t g = fk_probe_mode == 1 ? ld_value<COHERENT>(a.val + s.v[q], x.pl) : 0;
+            if ((int32_t)(s.p[q] + (uint32_t)s.wt[q]) < g || s.v[q] == 0xfffffffeu) acc.nu++;
+        }
+        return;
+    }
+#endif
+    int32_t cur[U];
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        cur[q] = 0;
+        if (s.ok[q]) {
+            if (ALGO == BFS) cur[q] = bit_test(a.vis, s.v[q]) ? 0 : INF;
+            else cur[q] = ld_value<COHERENT>(a.val + s.v[q], x.pl);
+        }
+    }
+    bool need[U];
+    uint32_t citem[U];
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        need[q] = false; citem[q] = 0;
+        if (!s.ok[q]) continue;
+        if (ALGO == SSSP) {
+            const uint32_t cand = s.p[q] + (uint32_t)s.wt[q];
+            if (cand >= (uint32_t)INF) {
+                acc.ovf = true;
+            } else if ((int32_t)cand < cur[q]) {
+                atomicMin(a.val + s.v[q], (int32_t)cand);   // result unused: RED.MIN
+                acc.nu++; acc.chg = true;
+                if (STYLE == DELTA && cand >= x.thr) {   // beyond the bucket: park in the far set
+                    atomicOr(a.vis + (s.v[q] >> 5), 1u << (s.v[q] & 31));
+                    x.pend_min = cand < x.pend_min ? cand : x.pend_min;
+                } else {
+                    need[q] = true; citem[q] = s.v[q];
+                }
+            }
+        } else if (ALGO == BFS) {
+            // t.dist > lev+1 -> t.dist = lev+1 (plain store;
+            // concurrent writers store the same value, R9)
+            if (cur[q] == INF) {
+                if (QUEUE) {   // the queue needs exactly-once: claim
+                    need[q] = true; citem[q] = s.v[q];
+                } else {   // the level is written when the vertex is expanded next round
+                    atomicOr(a.vis + (s.v[q] >> 5), 1u << (s.v[q] & 31));
+                    atomicOr(x.bm_now + (s.v[q] >> 5), 1u << (s.v[q] & 31));
+                    acc.nu++; acc.chg = true;
+                }
+            }
+        }
+    }
+    if (STYLE == VERTEX) {
+        if (ALGO == SSSP) {
+#pragma unroll
+            for (int q = 0; q < U; q++)
+                if (need[q]) atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
+        }
+    } else {
+        uint32_t got[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            got[q] = 0xffffffffu;
+            if (!need[q]) continue;
+            uint32_t *bmp = ALGO == BFS ? a.vis : x.bm_now;
+            got[q] = atomicOr(bmp + (citem[q] >> 5), 1u << (citem[q] & 31));
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
+            if (ALGO == BFS && want) {
+                a.val[citem[q]] = (int32_t)(x.lev + 1);
+                atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));   // dense rounds read it
+                acc.nu++; acc.chg = true;
+            }
+            const unsigned mask = __ballot_sync(FULL, want);
+            if (want) x.wq[x.qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
+            x.qn += __popc(mask);
+        }
+        __syncwarp();
+        if (x.qn > (uint32_t)(WQ > 32 * U ? WQ - 32 * U : 0)) {   // flush the staged appends
+            uint32_t b = 0;
+            if (lane == 0) b = atomicAdd(&x.c->out_len, x.qn);
+            b = __shfl_sync(FULL, b, 0);
+            for (uint32_t i = lane; i < x.qn; i += 32) x.out[b + i] = x.wq[i];
+            __syncwarp();
+            x.qn = 0;
+        }
+    }
+}
+
+// Relax the arcs of one 32-item tile (lane: value pay, arcs [beg, beg+deg)).
+// Software pipeline ACROSS tiles: each step's (col, w) loads are issued, then
+// the PREVIOUS step -- possibly of the previous tile -- gathers and relaxes.
+// With average degree ~4 a tile is a single step, so a per-tile pipeline
+// would expose two dependent latencies per tile (arcs, then gathered values;
+// ncu: 43 % of the stall samples); here the arc loads of tile t are in flight
+// while tile t-1's gathers are waited on.  The caller drains `pend` with
+// relax_step at the end of the round.
+template <int ALGO, int STYLE, int U, bool COHERENT>
+__device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, uint32_t deg, uint32_t pay,
+                                           RoundAcc &acc, Step<U> &pend) {
     const int lane = threadIdx.x & 31;
     uint32_t incl = deg;
 #pragma unroll
@@ -462,16 +579,13 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
     const uint32_t total = __shfl_sync(FULL, incl, 31);
     const uint32_t excl = incl - deg;
     if (lane == 0) acc.ne += total;
-
-    // Two-stage software pipeline over steps of 32*U arcs: the (col, w) loads
-    // of step i+1 are issued before the value gathers of step i are consumed,
-    // so each lane keeps 2U independent loads in flight.
-    auto stage1 = [&](uint32_t base, uint32_t (&v)[U], int32_t (&wt)[U], uint32_t (&p)[U], bool (&ok)[U]) {
+    for (uint32_t base = 0; base < total; base += 32 * U) {   // warp-uniform
+        Step<U> nx;
         uint32_t e[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
             const uint32_t k = base + q * 32 + lane;
-            ok[q] = k < total;
+            nx.ok[q] = k < total;
             int j = 0;
 #pragma unroll
             for (int st = 16; st > 0; st >>= 1) {
@@ -479,116 +593,24 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
                 if (ex <= k) j += st;
             }
             const uint32_t bj = __shfl_sync(FULL, beg, j), xj = __shfl_sync(FULL, excl, j);
-            p[q] = __shfl_sync(FULL, pay, j);
+            nx.p[q] = __shfl_sync(FULL, pay, j);
             e[q] = bj + (k - xj);
         }
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            v[q] = 0; wt[q] = 0;
-            if (ok[q]) {
+            nx.v[q] = 0; nx.wt[q] = 0;
+            if (nx.ok[q]) {
                 if (ALGO == SSSP) {   // one 8-byte (col, w) word
                     const uint2 w2 = ld_stream2(x.arcs + e[q], x.pf);
-                    v[q] = w2.x; wt[q] = (int32_t)w2.y;
+                    nx.v[q] = w2.x; nx.wt[q] = (int32_t)w2.y;
                 } else {
-                    v[q] = ld_stream(a.col + e[q], x.pf);
+                    nx.v[q] = ld_stream(a.col + e[q], x.pf);
                 }
             }
         }
-    };
-    uint32_t v[U], p[U];
-    int32_t wt[U];
-    bool ok[U];
-    if (total) stage1(0, v, wt, p, ok);
-    for (uint32_t base = 0; base < total; base += 32 * U) {   // warp-uniform
-        int32_t cur[U];
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            cur[q] = 0;
-            if (ok[q]) {
-                if (ALGO == BFS) cur[q] = bit_test(a.vis, v[q]) ? 0 : INF;
-                else cur[q] = ld_value<COHERENT>(a.val + v[q], x.pl);
-            }
-        }
-        uint32_t vn[U], pn[U];
-        int32_t wtn[U];
-        bool okn[U];
-        const bool more = base + 32 * U < total;
-        if (more) stage1(base + 32 * U, vn, wtn, pn, okn);
-        bool need[U];
-        uint32_t citem[U];
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            need[q] = false; citem[q] = 0;
-            if (!ok[q]) continue;
-            if (ALGO == SSSP) {
-                const uint32_t cand = p[q] + (uint32_t)wt[q];
-                if (cand >= (uint32_t)INF) {
-                    acc.ovf = true;
-                } else if ((int32_t)cand < cur[q]) {
-                    atomicMin(a.val + v[q], (int32_t)cand);   // result unused: RED.MIN
-                    acc.nu++; acc.chg = true;
-                    if (STYLE == DELTA && cand >= x.thr) {   // beyond the bucket: park in the far set
-                        atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
-                        x.pend_min = cand < x.pend_min ? cand : x.pend_min;
-                    } else {
-                        need[q] = true; citem[q] = v[q];
-                    }
-                }
-            } else if (ALGO == BFS) {
-                // t.dist > lev+1 -> t.dist = lev+1 (plain store;
-                // concurrent writers store the same value, R9)
-                if (cur[q] == INF) {
-                    if (QUEUE) {   // the queue needs exactly-once: claim
-                        need[q] = true; citem[q] = v[q];
-                    } else {   // the level is written when the vertex is expanded next round
-                        atomicOr(a.vis + (v[q] >> 5), 1u << (v[q] & 31));
-                        atomicOr(x.bm_now + (v[q] >> 5), 1u << (v[q] & 31));
-                        acc.nu++; acc.chg = true;
-                    }
-                }
-            }
-        }
-        if (STYLE == VERTEX) {
-            if (ALGO == SSSP) {
-#pragma unroll
-                for (int q = 0; q < U; q++)
-                    if (need[q]) atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
-            }
-        } else {
-            uint32_t got[U];
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                got[q] = 0xffffffffu;
-                if (!need[q]) continue;
-                uint32_t *bmp = ALGO == BFS ? a.vis : x.bm_now;
-                got[q] = atomicOr(bmp + (citem[q] >> 5), 1u << (citem[q] & 31));
-            }
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
-                if (ALGO == BFS && want) {
-                    a.val[citem[q]] = (int32_t)(x.lev + 1);
-                    atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));   // dense rounds read it
-                    acc.nu++; acc.chg = true;
-                }
-                const unsigned mask = __ballot_sync(FULL, want);
-                if (want) x.wq[x.qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
-                x.qn += __popc(mask);
-            }
-            __syncwarp();
-            if (x.qn > (uint32_t)(WQ > 32 * U ? WQ - 32 * U : 0)) {   // flush the staged appends
-                uint32_t b = 0;
-                if (lane == 0) b = atomicAdd(&x.c->out_len, x.qn);
-                b = __shfl_sync(FULL, b, 0);
-                for (uint32_t i = lane; i < x.qn; i += 32) x.out[b + i] = x.wq[i];
-                __syncwarp();
-                x.qn = 0;
-            }
-        }
-        if (more) {
-#pragma unroll
-            for (int q = 0; q < U; q++) { v[q] = vn[q]; wt[q] = wtn[q]; p[q] = pn[q]; ok[q] = okn[q]; }
-        }
+        if (pend.live) relax_step<ALGO, STYLE, U, COHERENT>(a, x, pend, acc);
+        pend = nx;
+        pend.live = true;
     }
 }
 
@@ -608,6 +630,8 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
     x.pf = pol_evict_first(); x.pl = pol_evict_last();
     blocked = blocked && ALGO == SSSP && a.nblk > 1;
     const uint32_t K = blocked ? a.nblk : 1u;
+    Step<U> pend;
+    pend.live = false;
 
     for (uint32_t k = 0; k < K; k++) {
         const bool first = k == 0, last = k + 1 == K;
@@ -647,7 +671,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                         if (ALGO == BFS && STYLE == VERTEX) a.val[u] = (int32_t)x.lev;   // discovered last round
                     }
                     if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-                    relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc);
+                    relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc, pend);
                 }
                 __syncwarp();
             }
@@ -668,10 +692,11 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                 if (QUEUE && last && u != NONE) x.bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
                 if (u != NONE && first) acc.nv++;
                 if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-                relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc);
+                relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc, pend);
             }
         }
     }
+    if (pend.live) relax_step<ALGO, STYLE, U, COHERENT>(a, x, pend, acc);   // drain the pipeline
     if (QUEUE) {
         __syncwarp();
         if (x.qn) {
