@@ -668,7 +668,8 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_persist;
-    for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_small, g->grid_cc, g->grid_pull})
+    for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_small, g->grid_cc,
+                    g->grid_pull})
         if (gsz > slots) slots = gsz;
     g->cnt_slots = slots;
     CU(dmalloc(&g->cnt, 3 * (size_t)slots));

@@ -805,13 +805,33 @@ __device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint3
     }
 }
 
-// A warp owns a chunk of ECH = 128*QP consecutive arcs (lane: QP quads, 16-byte
-// loads, consecutive lanes on consecutive quads).  The chunk's source range
-// [lo, hi] is precomputed at load time (k_chunk_range); when the activity
-// bitmap shows no active source in it, the warp skips the chunk without
-// reading src[] -- a sparse round streams 4 bytes of bitmap per 32 sources
-// instead of 4 bytes of src[] per arc.  In a dense round every arc's source
-// bit is tested.
+// EDGE style (COO).  A warp owns chunks of ECH = 128*QP
+// consecutive arcs (lane: QP quads, 16-byte loads, consecutive lanes on
+// consecutive quads).  Each chunk's source range [lo, hi] is precomputed at
+// load time (k_chunk_range), so liveness needs no src[] read: the warp checks
+// 32 chunks at once, one per lane (range -> the range's activity-bitmap words
+// -> ballot), and expands only the live ones -- a sparse round streams a few
+// bitmap words per 128 sources instead of 4 bytes of src[] per arc.  In a live
+// chunk every arc's source bit is tested and (col, w) fetched only for quads
+// with an active source.
+template <int ALGO, int QP>
+__device__ __forceinline__ void edge_load_src(const uint32_t *srcp, uint32_t ch, uint32_t m4, uint32_t nq,
+                                              uint32_t tail, uint64_t pf, uint32_t (&sq)[QP][4]) {
+    constexpr uint32_t ECH = 128u * QP;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int p = 0; p < QP; p++) {
+        const uint32_t q = ch * (ECH / 4) + p * 32 + lane;
+        sq[p][0] = sq[p][1] = sq[p][2] = sq[p][3] = 0;
+        if (q < m4) {
+            const uint4 s4 = ld_stream4(srcp + 4ull * q, pf);
+            sq[p][0] = s4.x; sq[p][1] = s4.y; sq[p][2] = s4.z; sq[p][3] = s4.w;
+        } else if (q < nq) {
+            for (uint32_t j = 0; j < tail; j++) sq[p][j] = ld_stream(srcp + 4ull * q + j, pf);
+        }
+    }
+}
+
 template <int ALGO, int B, int QP>
 __global__ void __launch_bounds__(B) k_edge(Args a) {
     static_assert(ALGO != CC, "CC has its own EDGE kernel (cc.cuh)");
@@ -832,40 +852,44 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
     const uint32_t nch = (a.m + ECH - 1) / ECH;
     unsigned long long ne = 0, nu = 0;
     bool chg = false, ovf = false;
-    for (uint32_t ch = gw; ch < nch; ch += nwarps) {   // warp-uniform
-        const uint2 r = rng[ch];
-        const uint32_t w0 = r.x >> 5, nw = (r.y >> 5) - w0 + 1;
-        if (nw <= 32) {   // one bitmap word per lane: skip the chunk if no source is active
-            const uint32_t word = (uint32_t)lane < nw ? bm_prev[w0 + lane] : 0u;
-            if (!__any_sync(FULL, word != 0u)) continue;
-        }
-        uint32_t sq[QP][4];
-        uint32_t act[QP];
-#pragma unroll
-        for (int p = 0; p < QP; p++) {
-            const uint32_t q = ch * (ECH / 4) + p * 32 + lane;
-            sq[p][0] = sq[p][1] = sq[p][2] = sq[p][3] = 0;
-            if (q < m4) {
-                const uint4 s4 = ld_stream4(srcp + 4ull * q, pf);
-                sq[p][0] = s4.x; sq[p][1] = s4.y; sq[p][2] = s4.z; sq[p][3] = s4.w;
-            } else if (q < nq) {
-                for (uint32_t j = 0; j < tail; j++) sq[p][j] = ld_stream(srcp + 4ull * q + j, pf);
+    for (uint32_t cb = gw; cb < nch; cb += 32 * nwarps) {   // warp-uniform: 32 chunks, one per lane
+        const uint32_t myc = cb + lane * nwarps;
+        bool live = false;
+        if (myc < nch) {
+            const uint2 r = rng[myc];
+            const uint32_t w0 = r.x >> 5, nw = (r.y >> 5) - w0 + 1;
+            if (nw > 32) {
+                live = true;
+            } else {   // a 512-arc chunk spans ~9 words on rand-25M's blocked order, up to 32 checked
+                uint32_t any = 0;
+#pragma unroll 8
+                for (uint32_t k = 0; k < nw; k++) any |= bm_prev[w0 + k];
+                live = any != 0;
             }
         }
+        unsigned mask = __ballot_sync(FULL, live);
+        if (!mask) continue;
+        while (mask) {   // warp-uniform over the live chunks of the batch
+            const uint32_t ch = cb + (__ffs(mask) - 1) * nwarps;
+            mask &= mask - 1;
+            uint32_t sq[QP][4];
+            edge_load_src<ALGO, QP>(srcp, ch, m4, nq, tail, pf, sq);
+            uint32_t act[QP];
 #pragma unroll
-        for (int p = 0; p < QP; p++) {
-            const uint32_t q = ch * (ECH / 4) + p * 32 + lane;
-            const uint32_t cntq = q < m4 ? 4u : (q < nq ? tail : 0u);
-            act[p] = 0;
+            for (int p = 0; p < QP; p++) {
+                const uint32_t q = ch * (ECH / 4) + p * 32 + lane;
+                const uint32_t cntq = q < m4 ? 4u : (q < nq ? tail : 0u);
+                act[p] = 0;
 #pragma unroll
-            for (int j = 0; j < 4; j++)   // the source must be active (improved / discovered last round)
-                if ((uint32_t)j < cntq && bit_test(bm_prev, sq[p][j])) act[p] |= 1u << j;
+                for (int j = 0; j < 4; j++)   // the source must be active (improved / discovered last round)
+                    if ((uint32_t)j < cntq && bit_test(bm_prev, sq[p][j])) act[p] |= 1u << j;
+            }
+#pragma unroll
+            for (int p = 0; p < QP; p++)
+                if (act[p])
+                    edge_quad<ALGO>(a, ch * (ECH / 4) + p * 32 + lane, sq[p], act[p], m4, tail, lev, bm_now, pf, pl,
+                                    ne, nu, chg, ovf);
         }
-#pragma unroll
-        for (int p = 0; p < QP; p++)
-            if (act[p])
-                edge_quad<ALGO>(a, ch * (ECH / 4) + p * 32 + lane, sq[p], act[p], m4, tail, lev, bm_now, pf, pl, ne,
-                                nu, chg, ovf);
     }
     flush_counters<B>(a, 0ull, ne, nu, chg, ovf);
 }
