@@ -28,8 +28,10 @@ namespace {
 
 constexpr int BLOCK = 256;
 constexpr int UNROLL = 4;   // arcs per thread per expansion step
-constexpr int EDGE_QP = 4;   // 4-arc quads per lane per chunk (EDGE style)
-constexpr uint32_t ECH = 128u * EDGE_QP;   // arcs per EDGE warp chunk
+// EDGE style: 4-arc quads per lane per warp chunk, per algorithm (measured on
+// B200: SSSP prefers short chunks -- 48 registers, 5 CTAs/SM; BFS longer ones)
+constexpr int EDGE_QP_SSSP = 1, EDGE_QP_BFS = 2;
+constexpr uint32_t ECH_SSSP = 128u * EDGE_QP_SSSP, ECH_BFS = 128u * EDGE_QP_BFS;   // arcs per warp chunk
 constexpr int HOST_CHECK_EVERY = 4;
 
 thread_local std::string g_last_error;
@@ -74,7 +76,8 @@ struct falcon_graph {
     uint2 *cw = nullptr;
     uint32_t *rowb = nullptr, *srcb = nullptr;   // destination-blocked layout (SSSP), built lazily
     uint2 *cwb = nullptr;
-    uint2 *chunk = nullptr, *chunkb = nullptr;   // EDGE chunk source ranges of src / srcb
+    uint2 *chunk = nullptr, *chunkb = nullptr;   // EDGE chunk source ranges: of src (BFS chunks) / srcb (SSSP chunks)
+    uint2 *chunks = nullptr;                     // ... of src in SSSP chunks (unblocked graphs)
     uint32_t nblk = 1, bsz = 0;
     size_t blk_bytes = 64u << 20;        // value-array bytes per block (FALCON_BLOCK_MB)
     uint32_t dense_div = 16;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV)
@@ -90,7 +93,7 @@ struct falcon_graph {
     unsigned long long *cnt = nullptr;
     int *d_flags = nullptr;
     int num_sms = 0;
-    int grid_persist = 0, grid_expand_fr = 0, grid_expand_dl = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_small = 0, cnt_slots = 0;
+    int grid_persist = 0, grid_expand_fr = 0, grid_expand_dl = 0, grid_pull = 0, grid_cc = 0, grid_edge = 0, grid_edge_b = 0, grid_small = 0, cnt_slots = 0;
     cudaGraph_t graphs[3][4] = {};
     cudaGraphExec_t execs[3][4] = {};
     int32_t delta = 0;                   // DELTA bucket width (0 = auto: max(1, average weight))
@@ -124,7 +127,7 @@ struct falcon_graph {
         a.cwb = blk ? cwb : a.cw;
         a.srcb = blk ? srcb : src;
         a.chunk = chunk;
-        a.chunkb = blk ? chunkb : chunk;
+        a.chunkb = blk ? chunkb : chunks;
         a.dense_div = dense_div;
         a.blk_div = blk_div;
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
@@ -241,7 +244,8 @@ struct Round {
             launch_expand_warp<ALGO, WORKLIST>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else {
-            launch_l2(g, k_edge<ALGO, BLOCK, EDGE_QP>, g->grid_edge, s, a);
+            if (ALGO == SSSP) launch_l2(g, k_edge<SSSP, BLOCK, EDGE_QP_SSSP>, g->grid_edge, s, a);
+            else launch_l2(g, k_edge<BFS, BLOCK, EDGE_QP_BFS>, g->grid_edge_b, s, a);
             if (tr) tr->mark(s, "edge", 0);
         }
         launches++;
@@ -313,9 +317,11 @@ falcon_status_t ensure_src(falcon_graph *g) {
         return FALCON_OK;
     }
     CU(dmalloc(&g->src, (size_t)g->m));
-    CU(dmalloc(&g->chunk, (size_t)((g->m + ECH - 1) / ECH)));
+    CU(dmalloc(&g->chunk, (size_t)((g->m + ECH_BFS - 1) / ECH_BFS)));
+    CU(dmalloc(&g->chunks, (size_t)((g->m + ECH_SSSP - 1) / ECH_SSSP)));
     k_build_src<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->n, (uint32_t)g->m, g->row_off, g->src);
-    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH, g->src, g->chunk);
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH_BFS, g->src, g->chunk);
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH_SSSP, g->src, g->chunks);
     CU(cudaGetLastError());
     return FALCON_OK;
 }
@@ -350,8 +356,8 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(g->rowb, len, tiles);
     k_blk_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->cw, bsz, (uint32_t)K, g->rowb, g->cwb,
                                                    g->srcb);
-    CU(dmalloc(&g->chunkb, (size_t)((m + ECH - 1) / ECH)));
-    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH, g->srcb, g->chunkb);
+    CU(dmalloc(&g->chunkb, (size_t)((m + ECH_SSSP - 1) / ECH_SSSP)));
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH_SSSP, g->srcb, g->chunkb);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));
     g->nblk = (uint32_t)K;
@@ -586,7 +592,7 @@ void destroy(falcon_graph *g) {
     if (g->ev1) cudaEventDestroy(g->ev1);
     cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->cw); cudaFree(g->src);
     cudaFree(g->rin_off); cudaFree(g->rin_col);
-    cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb); cudaFree(g->chunk); cudaFree(g->chunkb);
+    cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb); cudaFree(g->chunk); cudaFree(g->chunkb); cudaFree(g->chunks);
     cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1); cudaFree(g->tiles);
     cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
@@ -652,13 +658,16 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     g->persist = (pe && pe[0] == '1') && occ_p > 0;   // measured: no faster than per-round graph launches
     const char *pm = getenv("FALCON_PERSIST_MAX");
     if (pm) g->persist_max = (uint32_t)atoll(pm);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK, EDGE_QP>, BLOCK, 0));
+    int occ_eb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, k_edge<SSSP, BLOCK, EDGE_QP_SSSP>, BLOCK, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_eb, k_edge<BFS, BLOCK, EDGE_QP_BFS>, BLOCK, 0));
     auto clampg = [](int64_t want, int64_t cap) { return (int)(want < 1 ? 1 : (want > cap ? cap : want)); };
     auto full = [&](int occ) { return (int64_t)g->num_sms * (occ > 0 ? occ : 1); };
     g->grid_persist = (int)full(occ_p);
     g->grid_expand_fr = clampg((n + BLOCK - 1) / BLOCK, full(occ_f));
     g->grid_expand_dl = clampg((n + BLOCK - 1) / BLOCK, full(g->variant ? occ_f : 4));
-    g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP - 1) / (BLOCK * EDGE_QP), full(occ_e));
+    g->grid_edge = clampg((m / 4 + 1 + BLOCK * EDGE_QP_SSSP - 1) / (BLOCK * EDGE_QP_SSSP), full(occ_e));
+    g->grid_edge_b = clampg((m / 4 + 1 + BLOCK * EDGE_QP_BFS - 1) / (BLOCK * EDGE_QP_BFS), full(occ_eb));
     g->grid_small = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     g->grid_cc = clampg((n + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
@@ -668,7 +677,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     int slots = g->grid_persist;
-    for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_small, g->grid_cc,
+    for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_edge_b, g->grid_small, g->grid_cc,
                     g->grid_pull})
         if (gsz > slots) slots = gsz;
     g->cnt_slots = slots;

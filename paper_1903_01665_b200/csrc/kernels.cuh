@@ -82,8 +82,8 @@ struct Args {
     const uint32_t *rowb;      // [nblk*(n+1)]
     const uint2 *cwb;          // [m]
     const uint32_t *srcb;      // [m] EDGE style
-    const uint2 *chunk;        // [m/ECH] source range [min, max] of each EDGE chunk of src (CSR order)
-    const uint2 *chunkb;       // ... of srcb (blocked order)
+    const uint2 *chunk;        // source range [min, max] of each EDGE chunk of src (CSR order; BFS chunk size)
+    const uint2 *chunkb;       // ... of srcb (blocked order) or src, in SSSP chunks
     uint32_t nblk;
     uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
     uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
