@@ -82,6 +82,7 @@ struct falcon_graph {
     size_t blk_bytes = 64u << 20;        // value-array bytes per block (FALCON_BLOCK_MB)
     uint32_t dense_div = 16;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV)
     uint32_t blk_div = 8;                // blocked round: frontier > n / blk_div (FALCON_BLOCK_DIV)
+    uint32_t wl_noq = 1;                 // WORKLIST dense rounds without claims / queue (FALCON_WL_NOQ)
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     int32_t *val = nullptr;
@@ -117,7 +118,7 @@ struct falcon_graph {
     bool use_unit = false;
 
     Args args() const {
-        Args a;
+        Args a{};
         a.n = (uint32_t)n; a.m = (uint32_t)m; a.nwords = nwords;
         a.row_off = row_off; a.col = col; a.w = w; a.cw = use_unit ? cw_unit : cw; a.src = src;
         a.rin_off = rin_off; a.rin_col = rin_col;
@@ -130,6 +131,7 @@ struct falcon_graph {
         a.chunkb = blk ? chunkb : chunks;
         a.dense_div = dense_div;
         a.blk_div = blk_div;
+        a.wl_noq = wl_noq;
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
@@ -673,6 +675,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     g->grid_pull = clampg(((int64_t)g->nwords * 32 + BLOCK - 1) / BLOCK, (int64_t)g->num_sms * 8);
     if (const char *bmb = getenv("FALCON_BLOCK_MB")) g->blk_bytes = (size_t)atoll(bmb) << 20;   // 0: no blocking
     if (const char *dd = getenv("FALCON_DENSE_DIV")) g->dense_div = (uint32_t)atoi(dd);        // 0: never dense
+    if (const char *wq = getenv("FALCON_WL_NOQ")) g->wl_noq = (uint32_t)atoi(wq);
     if (const char *bd = getenv("FALCON_BLOCK_DIV")) g->blk_div = (uint32_t)atoi(bd);          // 0: never blocked
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
@@ -861,6 +864,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->dense_div = (uint32_t)value;
         } else if (!strcmp(name, "block_div")) {
             t->blk_div = (uint32_t)value;
+        } else if (!strcmp(name, "wl_noq")) {
+            t->wl_noq = (uint32_t)(value != 0);
         } else if (!strcmp(name, "pull_div")) {
             t->pull_div = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {

@@ -62,6 +62,8 @@ struct Ctrl {
     uint32_t bar_arrive;  // persistent kernel: CTAs arrived at the grid barrier
     uint32_t bar_gen;     // persistent kernel: barrier generation
     uint32_t blk;         // this round expands over the destination-blocked layout (dense rounds)
+    uint32_t noq;         // WORKLIST: this (dense) round marks the bitmap only -- no queue is built
+    uint32_t prevnoq;     // WORKLIST: the previous round did: read this round's items from the bitmap
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
     unsigned long long edges;
@@ -87,6 +89,7 @@ struct Args {
     uint32_t nblk;
     uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
     uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
+    uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
@@ -254,7 +257,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
         c->pull = 0; c->found = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
-        c->bar_arrive = 0; c->blk = 0;
+        c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
 }
@@ -459,10 +462,12 @@ struct Step {
     bool live;
 };
 
-// Gather the targets' values of a loaded step and relax its arcs.
-template <int ALGO, int STYLE, int U, bool COHERENT>
+// Gather the targets' values of a loaded step and relax its arcs.  NOQ: a
+// dense WORKLIST round marks improved vertices like VERTEX does (reductions,
+// no claim, no queue append): its successor reads the frontier from the bitmap.
+template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false>
 __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &s, RoundAcc &acc) {
-    constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
+    constexpr bool QUEUE = (STYLE == WORKLIST || STYLE == DELTA) && !NOQ;
     constexpr int WQ = QUEUE ? 256 : 1;
     const int lane = threadIdx.x & 31;
 #ifdef FK_PROBE   // tools/expand_probe.cu: time the expansion without (0) / with (1) the gathers
@@ -511,15 +516,16 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
             if (cur[q] == INF) {
                 if (QUEUE) {   // the queue needs exactly-once: claim
                     need[q] = true; citem[q] = s.v[q];
-                } else {   // the level is written when the vertex is expanded next round
+                } else {   // VERTEX: the level is written when the vertex is expanded next round
                     atomicOr(a.vis + (s.v[q] >> 5), 1u << (s.v[q] & 31));
                     atomicOr(x.bm_now + (s.v[q] >> 5), 1u << (s.v[q] & 31));
+                    if (NOQ) a.val[s.v[q]] = (int32_t)(x.lev + 1);
                     acc.nu++; acc.chg = true;
                 }
             }
         }
     }
-    if (STYLE == VERTEX) {
+    if (!QUEUE) {
         if (ALGO == SSSP) {
 #pragma unroll
             for (int q = 0; q < U; q++)
@@ -566,7 +572,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
 // ncu: 43 % of the stall samples); here the arc loads of tile t are in flight
 // while tile t-1's gathers are waited on.  The caller drains `pend` with
 // relax_step at the end of the round.
-template <int ALGO, int STYLE, int U, bool COHERENT>
+template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ>
 __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, uint32_t deg, uint32_t pay,
                                            RoundAcc &acc, Step<U> &pend) {
     const int lane = threadIdx.x & 31;
@@ -608,7 +614,7 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
                 }
             }
         }
-        if (pend.live) relax_step<ALGO, STYLE, U, COHERENT>(a, x, pend, acc);
+        if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ>(a, x, pend, acc);
         pend = nx;
         pend.live = true;
     }
@@ -616,7 +622,7 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
 
 // One round of expansion by this warp.  sit: the warp's 1024-entry shared
 // item list (dense rounds).
-template <int ALGO, int STYLE, int U, bool COHERENT>
+template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false>
 __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, const uint32_t *in,
                                              uint32_t *out, uint32_t nitems, bool dense, bool blocked, uint32_t *wq,
                                              uint32_t *sit, RoundAcc &acc) {
@@ -671,7 +677,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                         if (ALGO == BFS && STYLE == VERTEX) a.val[u] = (int32_t)x.lev;   // discovered last round
                     }
                     if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-                    relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc, pend);
+                    relax_tile<ALGO, STYLE, U, COHERENT, NOQ>(a, x, beg, deg, pay, acc, pend);
                 }
                 __syncwarp();
             }
@@ -692,12 +698,12 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                 if (QUEUE && last && u != NONE) x.bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
                 if (u != NONE && first) acc.nv++;
                 if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-                relax_tile<ALGO, STYLE, U, COHERENT>(a, x, beg, deg, pay, acc, pend);
+                relax_tile<ALGO, STYLE, U, COHERENT, NOQ>(a, x, beg, deg, pay, acc, pend);
             }
         }
     }
-    if (pend.live) relax_step<ALGO, STYLE, U, COHERENT>(a, x, pend, acc);   // drain the pipeline
-    if (QUEUE) {
+    if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ>(a, x, pend, acc);   // drain the pipeline
+    if (QUEUE && !NOQ) {
         __syncwarp();
         if (x.qn) {
             uint32_t b = 0;
@@ -737,8 +743,19 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     __shared__ uint32_t s_q[B / 32][WQ];
     __shared__ uint32_t s_it[B / 32][1024];
     RoundAcc acc;
-    expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems, dense, blocked, s_q[threadIdx.x >> 5],
-                                        s_it[threadIdx.x >> 5], acc);
+    if (STYLE == WORKLIST && dense && a.wl_noq) {
+        // dense WORKLIST round: items from the bitmap, improved vertices marked
+        // in the next bitmap with reductions -- no claim atomics, no queue.  The
+        // next round reads its items from that bitmap (Ctrl::prevnoq); if it is
+        // sparse, it builds the queue again with claims.
+        if (blockIdx.x == 0 && threadIdx.x == 0) c->noq = 1;
+        expand_round<ALGO, STYLE, U, false, true>(a, c, iter, thr, in, out, nitems, true, blocked,
+                                                  s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
+    } else {
+        expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems,
+                                            dense || (STYLE == WORKLIST && c->prevnoq), blocked,
+                                            s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
+    }
     flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
 }
 
@@ -941,7 +958,7 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
                                              uint32_t blk_div) {
     if (c->done) return false;
     c->launches += launches_per_round;
-    bool more = STYLE == WORKLIST ? c->out_len > 0 : c->changed != 0;
+    bool more = STYLE == WORKLIST ? (c->noq ? c->changed != 0 : c->out_len > 0) : c->changed != 0;
     if (STYLE == DELTA) {
         if (c->mode == MODE_SCAN) {
             more = true;                 // the refilled near queue (possibly empty) comes next
@@ -964,7 +981,11 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
         c->iter++;
         c->changed = 0;
         if (STYLE == WORKLIST || (STYLE == DELTA && c->mode == MODE_NEAR)) {
-            c->in_len = c->out_len;
+            // after a no-queue round the frontier size is estimated by the
+            // filter passes (>= the improved vertices): it only decides dense
+            c->in_len = STYLE == WORKLIST && c->noq ? c->found : c->out_len;
+            c->prevnoq = c->noq;
+            c->noq = 0;
             c->out_len = 0;
             c->sel ^= 1u;
             c->all_active = 0;
@@ -1039,6 +1060,7 @@ __global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div, uin
         if (ldv(&c->done)) break;
         const bool scan = STYLE == DELTA && ldv(&c->mode) == MODE_SCAN;
         if (!scan && ldv(&c->in_len) > max_items) break;
+        if (STYLE == WORKLIST && ldv(&c->prevnoq)) break;   // frontier only in the bitmap: k_expand_warp
         const uint32_t iter = ldv(&c->iter), sel = ldv(&c->sel);
         const uint32_t thr = STYLE == DELTA ? ldv(&c->thr) : 0xffffffffu;
         const uint32_t *in = sel ? a.fr1 : a.fr0;

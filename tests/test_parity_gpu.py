@@ -134,6 +134,25 @@ def test_parity_layouts(gpu_lib, name, layout, algo):
         assert np.array_equal(out2, exp), f"{name}/{algo}/{style}/{layout} (rerun)"
 
 
+@pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s", "ragged", "tiny"])
+@pytest.mark.parametrize("dense_div", [16, 10**6, 1])
+@pytest.mark.parametrize("wl_noq", [0, 1])
+@pytest.mark.parametrize("persist", [0, 1])
+def test_parity_worklist_noq(gpu_lib, name, dense_div, wl_noq, persist):
+    """WORKLIST dense rounds without claims / queue (frontier handed on in the
+    bitmap, rebuilt as a queue when the next round is sparse) reach the same
+    fixpoint, with and without persistent small rounds."""
+    G = _graph(name)
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    gpu_lib.falcon_set_option(g, "dense_div", dense_div)
+    gpu_lib.falcon_set_option(g, "wl_noq", wl_noq)
+    gpu_lib.falcon_set_option(g, "persist", persist)
+    for algo in ("sssp", "bfs"):
+        exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+        out, _ = _run(gpu_lib, g, algo, "worklist", G.source)
+        assert np.array_equal(out, exp), f"{name}/{algo}/dd={dense_div}/noq={wl_noq}: {np.flatnonzero(out != exp)[:10]}"
+
+
 def test_set_option_rejects_unknown(gpu_lib):
     G = _graph("tiny")
     g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
