@@ -849,6 +849,9 @@ __device__ __forceinline__ void edge_load_src(const uint32_t *srcp, uint32_t ch,
     }
 }
 
+#ifndef EDGE_PREFETCH
+#define EDGE_PREFETCH 1
+#endif
 template <int ALGO, int B, int QP>
 __global__ void __launch_bounds__(B) k_edge(Args a) {
     static_assert(ALGO != CC, "CC has its own EDGE kernel (cc.cuh)");
@@ -886,11 +889,16 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
         }
         unsigned mask = __ballot_sync(FULL, live);
         if (!mask) continue;
-        while (mask) {   // warp-uniform over the live chunks of the batch
-            const uint32_t ch = cb + (__ffs(mask) - 1) * nwarps;
+        uint32_t sq[QP][4];
+        uint32_t ch = cb + (__ffs(mask) - 1) * nwarps;
+        mask &= mask - 1;
+        edge_load_src<ALGO, QP>(srcp, ch, m4, nq, tail, pf, sq);
+        for (;;) {   // warp-uniform over the live chunks of the batch
+            // the next live chunk's sources are loaded while this one is relaxed
+            const uint32_t chn = mask ? cb + (__ffs(mask) - 1) * nwarps : NONE;
             mask &= mask - 1;
-            uint32_t sq[QP][4];
-            edge_load_src<ALGO, QP>(srcp, ch, m4, nq, tail, pf, sq);
+            uint32_t sqn[QP][4];
+            if (EDGE_PREFETCH && chn != NONE) edge_load_src<ALGO, QP>(srcp, chn, m4, nq, tail, pf, sqn);
             uint32_t act[QP];
 #pragma unroll
             for (int p = 0; p < QP; p++) {
@@ -906,6 +914,16 @@ __global__ void __launch_bounds__(B) k_edge(Args a) {
                 if (act[p])
                     edge_quad<ALGO>(a, ch * (ECH / 4) + p * 32 + lane, sq[p], act[p], m4, tail, lev, bm_now, pf, pl,
                                     ne, nu, chg, ovf);
+            if (chn == NONE) break;
+            ch = chn;
+            if (EDGE_PREFETCH) {
+#pragma unroll
+                for (int p = 0; p < QP; p++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) sq[p][j] = sqn[p][j];
+            } else {
+                edge_load_src<ALGO, QP>(srcp, ch, m4, nq, tail, pf, sq);
+            }
         }
     }
     flush_counters<B>(a, 0ull, ne, nu, chg, ovf);

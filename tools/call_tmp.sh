@@ -1,5 +1,8 @@
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "not full_config and not three_passes" > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
-for Q in 1 0; do
-FALCON_WL_NOQ=$Q timeout 900 python tools/survey.py --algos sssp,bfs --styles worklist --reps 3 2>&1 | grep -v "==" | sed "s/^/noq=$Q /"
-done > gpurun_out/survey_noq.log
+cp paper_1903_01665_b200/libfalcon.so /tmp/libfalcon_pf.so
+for V in pf nopf; do
+cp /tmp/libfalcon_pf.so paper_1903_01665_b200/libfalcon.so
+[ $V = nopf ] && cp paper_1903_01665_b200/libfalcon_nopf.so paper_1903_01665_b200/libfalcon.so
+timeout 600 python tools/survey.py --algos sssp,bfs --styles edge --reps 3 2>&1 | grep -v "==" | sed "s/^/$V /"
+done
+cp /tmp/libfalcon_pf.so paper_1903_01665_b200/libfalcon.so
+timeout 900 python -m pytest tests -m gpu -x -q -k "not full_config and not three_passes" 2>&1 | tail -1
