@@ -10,7 +10,12 @@
 // style) and cached.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <cstdarg>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -56,11 +61,74 @@ falcon_status_t fail(falcon_status_t st, const char *fmt, ...) {
         }                                                                                             \
     } while (0)
 
+// Device memory: a per-process caching allocator over cudaMalloc.  A freed
+// block (graph_free, per-call staging buffers) goes back to a cache keyed by
+// (device, size class) instead of to cudaFree -- which synchronises the device
+// and unmaps, ~7 ms for one rand-25M graph -- and the next allocation of that
+// class reuses it (the next graph of the same shape, the next call's
+// staging).  Size classes: 256 B below 1 MiB, 2 MiB above.  When cudaMalloc
+// fails the device's cached blocks are released and the allocation retried.
+// Callers free a block only after the work that uses it has completed.
+struct DevCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void *> idle;    // (device, bytes) -> block
+    std::unordered_map<void *, std::pair<int, size_t>> live;
+};
+DevCache &dev_cache() {
+    static DevCache *c = new DevCache();   // never destroyed: blocks may be freed during process exit
+    return *c;
+}
+
+cudaError_t dev_alloc(void **p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t gran = bytes < (1u << 20) ? 256 : (2u << 20);
+    bytes = (bytes + gran - 1) / gran * gran;
+    DevCache &c = dev_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.idle.find({dev, bytes});
+        if (it != c.idle.end()) {
+            *p = it->second;
+            c.idle.erase(it);
+            c.live[*p] = {dev, bytes};
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(p, bytes);   // 256-byte aligned: the 16-byte vector loads rely on it
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        std::vector<void *> rel;
+        {
+            std::lock_guard<std::mutex> lk(c.mu);
+            for (auto it = c.idle.begin(); it != c.idle.end();) {
+                if (it->first.first == dev) { rel.push_back(it->second); it = c.idle.erase(it); }
+                else ++it;
+            }
+        }
+        for (void *q : rel) cudaFree(q);
+        e = cudaMalloc(p, bytes);
+    }
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.live[*p] = {dev, bytes};
+    }
+    return e;
+}
+
+void dfree(void *p) {
+    if (!p) return;
+    DevCache &c = dev_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.live.find(p);
+    if (it == c.live.end()) return;
+    c.idle.insert({it->second, p});
+    c.live.erase(it);
+}
+
 template <typename T>
 cudaError_t dmalloc(T **p, size_t count) {
-    // cudaMalloc returns 256-byte aligned memory: the 16-byte vector loads
-    // of the EDGE kernel and the uint4 tile loads rely on it.
-    return cudaMalloc(reinterpret_cast<void **>(p), (count ? count : 1) * sizeof(T));
+    return dev_alloc(reinterpret_cast<void **>(p), (count ? count : 1) * sizeof(T));
 }
 
 }  // namespace
@@ -367,28 +435,40 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     return FALCON_OK;
 }
 
-// Reverse CSR for bottom-up BFS (built once, on the device).
+// Reverse CSR (in-arcs: BFS pull, CC worklist), built once on the device:
+// in-degree histogram + scan for the offsets, and a stable LSD radix sort of
+// the (target, source) arc pairs by target (CUB) for the in-neighbours -- the
+// in-row of v lists its sources in ascending order.
 falcon_status_t ensure_reverse(falcon_graph *g) {
     if (g->rin_off) return FALCON_OK;
     const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
     cudaStream_t s = g->stream;
     CU(dmalloc(&g->rin_off, n + 1));
     CU(dmalloc(&g->rin_col, m));
-    uint32_t *cursor = g->fr1, *tiles = g->tiles;   // load-time scratch (no run is in flight)
+    uint32_t *tiles = g->tiles;
     const uint32_t ntiles = (uint32_t)((n + 1 + 1023) / 1024);
     CU(cudaMemsetAsync(g->rin_off, 0, (n + 1) * 4, s));
     if (m) k_indeg<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->col, g->rin_off);
     k_scan_local<<<ntiles, 256, 0, s>>>(g->rin_off, n + 1, tiles);
     k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
     k_scan_add<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(g->rin_off, n + 1, tiles);
-    CU(cudaMemcpyAsync(cursor, g->rin_off, (n + 1) * 4, cudaMemcpyDeviceToDevice, s));
     if (m) {
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
-        const uint64_t win = 8u << 20;   // targets per pass: 32 MB of cursors
-        for (uint64_t lo = 0; lo < n; lo += win)
-            k_rev_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->src, g->col, cursor, g->rin_col, (uint32_t)lo,
-                                                           (uint32_t)(lo + win < n ? lo + win : n));
+        int end_bit = 1;
+        while (end_bit < 32 && (1ull << end_bit) < n) end_bit++;
+        uint32_t *keys_out = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_bytes = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, g->col, keys_out, g->src, g->rin_col, (int64_t)m, 0,
+                                           end_bit, s));
+        CU(dmalloc(&keys_out, m));
+        CU(dev_alloc(&tmp, tmp_bytes));
+        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, g->col, keys_out, g->src, g->rin_col, (int64_t)m, 0,
+                                           end_bit, s));
+        CU(cudaStreamSynchronize(s));
+        dfree(keys_out);
+        dfree(tmp);
     }
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));
@@ -447,7 +527,7 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
                 if (g->m) k_sum_weights<<<g->num_sms * 8, BLOCK, 0, s>>>((uint64_t)g->m, g->w, d_sum);
                 CU(cudaMemcpyAsync(&h_sum, d_sum, sizeof h_sum, cudaMemcpyDeviceToHost, s));
                 CU(cudaStreamSynchronize(s));
-                cudaFree(d_sum);
+                dfree(d_sum);
                 const unsigned long long avg = g->m ? h_sum / (unsigned long long)g->m : 1;
                 g->delta_auto = (int32_t)(avg < 1 ? 1 : (avg > 0x3fffffff ? 0x3fffffff : avg));
             }
@@ -592,11 +672,12 @@ void destroy(falcon_graph *g) {
     for (auto e : g->pev) cudaEventDestroy(e);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
-    cudaFree(g->row_off); cudaFree(g->col); cudaFree(g->w); cudaFree(g->cw); cudaFree(g->src);
-    cudaFree(g->rin_off); cudaFree(g->rin_col);
-    cudaFree(g->rowb); cudaFree(g->cwb); cudaFree(g->srcb); cudaFree(g->chunk); cudaFree(g->chunkb); cudaFree(g->chunks);
-    cudaFree(g->val); cudaFree(g->bm); cudaFree(g->fr0); cudaFree(g->fr1); cudaFree(g->tiles);
-    cudaFree(g->ctrl); cudaFree(g->cnt); cudaFree(g->d_flags);
+    for (void *p : {(void *)g->row_off, (void *)g->col, (void *)g->w, (void *)g->cw, (void *)g->src,
+                    (void *)g->rin_off, (void *)g->rin_col, (void *)g->rowb, (void *)g->cwb, (void *)g->srcb,
+                    (void *)g->chunk, (void *)g->chunkb, (void *)g->chunks, (void *)g->val, (void *)g->bm,
+                    (void *)g->fr0, (void *)g->fr1, (void *)g->tiles, (void *)g->ctrl, (void *)g->cnt,
+                    (void *)g->d_flags})
+        dfree(p);   // back to the device cache (the stream was synchronised above)
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
     if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
@@ -857,7 +938,7 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
     for (falcon_graph *t : targets) {
         if (!strcmp(name, "block_bytes")) {
             if (t->stream) cudaStreamSynchronize(t->stream);
-            cudaFree(t->rowb); cudaFree(t->cwb); cudaFree(t->srcb); cudaFree(t->chunkb);
+            dfree(t->rowb); dfree(t->cwb); dfree(t->srcb); dfree(t->chunkb);
             t->rowb = nullptr; t->cwb = nullptr; t->srcb = nullptr; t->chunkb = nullptr; t->nblk = 1; t->bsz = 0;
             t->blk_bytes = (size_t)value;
         } else if (!strcmp(name, "dense_div")) {

@@ -1174,30 +1174,6 @@ __global__ void k_scan_add(uint32_t *x, uint64_t len, const uint32_t *tile_sums)
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < len) x[i] += tile_sums[i / 1024];
 }
-// arc-parallel scatter of the COO arcs into the in-rows (in-row order is
-// arbitrary: BFS levels and CC labels do not depend on it).  One pass per
-// window of targets [lo, hi): the window's cursors (<= 32 MB) stay
-// L2-resident, so the position atomics run at L2 rate instead of missing to
-// DRAM; col[] is streamed once per window (evict-first).
-__global__ void k_rev_scatter(uint64_t m, const uint32_t *src, const uint32_t *col, uint32_t *cursor,
-                              uint32_t *rin_col, uint32_t lo, uint32_t hi) {
-    const uint64_t pf = pol_evict_first();
-    const uint64_t m4 = m >> 2;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= m4; q += stride) {
-        uint32_t c[4] = {hi, hi, hi, hi};
-        if (q < m4) {
-            const uint4 c4 = ld_stream4(col + 4 * q, pf);
-            c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-        } else {
-            for (uint64_t j = 0; 4 * q + j < m; j++) c[j] = col[4 * q + j];
-        }
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-            if (c[j] >= lo && c[j] < hi) rin_col[atomicAdd(cursor + c[j], 1u)] = ld_stream(src + 4 * q + j, pf);
-    }
-}
-
 __global__ void k_fill_i32(int32_t *p, uint64_t len, int32_t x) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) p[i] = x;

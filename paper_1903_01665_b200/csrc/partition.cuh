@@ -158,8 +158,9 @@ void destroy(falcon_graph *g);
 void destroy_partitioned(falcon_graph *g) {
     for (auto *p : g->parts) {
         cudaSetDevice(p->device);
-        cudaFree(p->recv);
-        cudaFree(p->cw_unit);
+        if (p->stream) cudaStreamSynchronize(p->stream);
+        dfree(p->recv);
+        dfree(p->cw_unit);
         p->recv = nullptr;
         p->cw_unit = nullptr;
         destroy(p);
@@ -193,7 +194,7 @@ falcon_status_t load_part(int64_t n, const uint32_t *h_row_off, const uint32_t *
         k_fill_i32<<<p->num_sms * 8, BLOCK, 0, p->stream>>>(ones, (uint64_t)mp, 1);
         k_interleave<<<p->num_sms * 8, BLOCK, 0, p->stream>>>((uint64_t)mp, p->col, ones, p->cw_unit);
         CU(cudaStreamSynchronize(p->stream));
-        cudaFree(ones);
+        dfree(ones);
     }
     *out = p;
     return FALCON_OK;
@@ -366,9 +367,9 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
     for (size_t i = 0; i < g->parts.size(); i++)
         CU(cudaMemcpyAsync(&hc[i], g->parts[i]->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    if (staging) cudaFree(staging);
-    if (d_vals) cudaFree(d_vals);
-    if (d_ctrls) cudaFree(d_ctrls);
+    dfree(staging);
+    dfree(d_vals);
+    dfree(d_ctrls);
     for (auto *p : g->parts) p->use_unit = false;
     if (stats) {
         float ms = 0.f;
