@@ -30,7 +30,7 @@ subprocess.run(["cp", os.path.join(src, "launches.csv"), os.path.join(prof, f"{t
 # dominant relax kernel's template name in the launch list
 algo, style = kernel.split("/")
 ai = {"sssp": 0, "bfs": 1, "cc": 2}[algo]
-name = {"edge": f"k_edge<{ai}, 256, 4>", "vertex": f"k_expand_warp<{ai}, 0,", "worklist": f"k_expand_warp<{ai}, 2,"}[style]
+name = {"edge": f"k_edge<{ai}, 256,", "vertex": f"k_expand_warp<{ai}, 0,", "worklist": f"k_expand_warp<{ai}, 2,"}[style]
 names, L = launches.load(os.path.join(src, "launches.csv"))
 sel = [L[k] for k in L if name in names[k]]
 traffic = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in sel) / max(1, len(sel))
