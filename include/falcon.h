@@ -143,8 +143,41 @@ FALCON_API falcon_status_t falcon_comm_free(falcon_comm_t *comm);
  * simulated graph). */
 FALCON_API falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi);
 
-/* Release all device memory of the graph.  NULL is a no-op. */
+/* Release the graph's device memory (to the library's device-memory cache,
+ * which later loads reuse; a failed allocation releases the cache).  NULL is a
+ * no-op.  Errors: INVALID_ARG if views created by graph_share are still live. */
 FALCON_API falcon_status_t graph_free(falcon_graph_t *g);
+
+/* A view of g for concurrent calls: it shares g's read-only graph arrays
+ * (CSR, COO, chunk ranges, blocked and reverse layouts -- all built now, on g)
+ * and owns its own scratch (value array, bitmaps, queues, control block,
+ * stream, cached CUDA graphs).  Calls on g and on each of its views may then
+ * run at the same time, from different host threads or through
+ * falcon_run_many -- the paper's concurrent BFS/SSSP kernels
+ * (PAPER.md:1040-1064, 1137-1142 §"Synchronous vs asynchronous").  opts:
+ * nullable; only cuda_stream is used (NULL = a stream the view owns).  A view
+ * of a view shares the root graph.  Free views (graph_free) before g.
+ * Errors: INVALID_ARG (NULL), UNSUPPORTED (partitioned g), NO_MEMORY, CUDA. */
+FALCON_API falcon_status_t graph_share(falcon_graph_t *g, const falcon_load_opts_t *opts, falcon_graph_t **out);
+
+typedef enum { FALCON_ALGO_SSSP = 0, FALCON_ALGO_BFS = 1, FALCON_ALGO_CC = 2 } falcon_algo_t;
+
+typedef struct {
+    falcon_algo_t algo;
+    falcon_style_t style;
+    uint32_t source; /* ignored for CC */
+} falcon_job_t;
+
+/* Run njobs calls concurrently: job i runs on graphs[i] (distinct handles --
+ * a graph and its views) and writes outs[i] (host|device int32[n]); every job
+ * is launched on its handle's stream before any is waited on.  stats: NULL or
+ * falcon_stats_t[njobs].  Returns when all jobs are complete; on error the
+ * first failing job's status (all launched jobs are still completed).
+ * Results equal those of the one-at-a-time calls.
+ * Errors: INVALID_ARG (NULL arrays, repeated handle, unknown algo/style,
+ * source >= n), UNSUPPORTED (partitioned graph), plus the per-call statuses. */
+FALCON_API falcon_status_t falcon_run_many(int njobs, falcon_graph_t *const *graphs, const falcon_job_t *jobs,
+                                           int32_t *const *outs, falcon_stats_t *stats);
 
 /* Query vertex / arc counts of a loaded graph. */
 FALCON_API falcon_status_t graph_info(const falcon_graph_t *g, int64_t *n, int64_t *m);
@@ -191,7 +224,10 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *   "persist_max"  ... while the frontier holds at most this many items
  * Changing an option drops the cached CUDA graphs (and, for block_bytes, the
  * blocked layout); they are rebuilt on the next call.
- * Errors: INVALID_ARG (g/name NULL, value out of range), UNSUPPORTED (unknown name). */
+ *   "wl_noq"       WORKLIST dense rounds mark the next bitmap without claims
+ *                  or a queue (default 1, env FALCON_WL_NOQ; 0 = off)
+ * Errors: INVALID_ARG (g/name NULL, value out of range), UNSUPPORTED (unknown
+ * name; block_bytes of a graph that has, or is, a view). */
 FALCON_API falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t value);
 
 /* Profiling mode (off by default): when on, the fixpoint loop is driven from

@@ -6,7 +6,7 @@ every call raises.  Arrays may be numpy arrays (host) or torch tensors (host
 or CUDA); PyTorch is used only for device memory and streams.
 
 Names follow the C ABI: graph_load_csr, graph_free, graph_info, graph_owned_range,
-falcon_sssp, falcon_bfs, falcon_cc, falcon_set_profiling, falcon_set_delta, falcon_set_option,
+graph_share, falcon_run_many, falcon_sssp, falcon_bfs, falcon_cc, falcon_set_profiling, falcon_set_delta, falcon_set_option,
 falcon_partition, falcon_comm_unique_id, falcon_comm_init,
 falcon_comm_init_simulated, falcon_comm_free, falcon_last_error, falcon_version.
 """
@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "falcon_sssp", "falcon_bfs", "falcon_cc",
+__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "graph_share", "falcon_run_many", "falcon_sssp", "falcon_bfs", "falcon_cc",
            "falcon_set_profiling", "falcon_set_delta", "falcon_set_option", "falcon_partition", "falcon_comm_unique_id",
            "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_free", "graph_owned_range", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
@@ -24,6 +24,7 @@ INF = 2147483647
 STYLE_VERTEX, STYLE_EDGE, STYLE_WORKLIST, STYLE_DELTA = 0, 1, 2, 3
 STYLES = {"vertex": STYLE_VERTEX, "edge": STYLE_EDGE, "worklist": STYLE_WORKLIST, "delta": STYLE_DELTA}
 LOAD_BUILD_COO = 0x1
+ALGOS = {"sssp": 0, "bfs": 1, "cc": 2}
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "NO_MEMORY", 4: "CUDA", 5: "OVERFLOW",
           6: "NOT_CONVERGED", 7: "COMM", 8: "UNSUPPORTED"}
 
@@ -47,6 +48,10 @@ class FalconStats(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class _Job(ctypes.Structure):
+    _fields_ = [("algo", ctypes.c_int), ("style", ctypes.c_int), ("source", ctypes.c_uint32)]
 
 
 class _LoadOpts(ctypes.Structure):
@@ -84,6 +89,11 @@ def load(build_if_missing: bool = False):
     lib.falcon_comm_init_simulated.argtypes = [ctypes.c_int, ctypes.POINTER(p)]
     lib.falcon_comm_free.argtypes = [p]
     lib.graph_owned_range.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.graph_share.argtypes = [p, ctypes.POINTER(_LoadOpts), ctypes.POINTER(p)]
+    lib.graph_share.restype = st
+    lib.falcon_run_many.argtypes = [ctypes.c_int, ctypes.POINTER(p), ctypes.POINTER(_Job), ctypes.POINTER(p),
+                                    ctypes.POINTER(FalconStats)]
+    lib.falcon_run_many.restype = st
     for f in (lib.falcon_partition, lib.falcon_comm_unique_id, lib.falcon_comm_init, lib.falcon_comm_init_simulated,
               lib.falcon_comm_free, lib.graph_owned_range):
         f.restype = st
@@ -144,6 +154,9 @@ class Graph:
     def __del__(self):
         try:
             graph_free(self)
+            parent = getattr(self, "_parent", None)
+            if parent is not None:
+                parent._views -= 1
         except Exception:
             pass
 
@@ -227,8 +240,35 @@ def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, strea
 
 def graph_free(g: Graph):
     if g is not None and g.handle:
-        load().graph_free(g.handle)
+        _check(load().graph_free(g.handle))
         g.handle = None
+
+
+def graph_share(g: Graph, stream=None) -> Graph:
+    """A view of g with its own scratch (for concurrent calls); free it before g."""
+    if stream is not None and hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    opts = _LoadOpts(-1, ctypes.c_void_p(stream) if stream else None, 0, None)
+    out = ctypes.c_void_p()
+    _check(load().graph_share(g.handle, ctypes.byref(opts), ctypes.byref(out)))
+    v = Graph(out, g.n, g.m)
+    v._parent = g   # the parent must outlive the view
+    g._views = getattr(g, "_views", 0) + 1
+    return v
+
+
+def falcon_run_many(jobs) -> list:
+    """Run jobs concurrently: jobs = [(graph, algo, style, source, out), ...] on
+    distinct handles (a graph and its views).  Returns one FalconStats per job."""
+    k = len(jobs)
+    hs = (ctypes.c_void_p * k)(*[j[0].handle for j in jobs])
+    js = (_Job * k)(*[_Job(ALGOS[j[1]], _style(j[2]), int(j[3])) for j in jobs])
+    for j in jobs:
+        _check_dtype(j[4], "i32", "out")
+    outs = (ctypes.c_void_p * k)(*[_ptr(j[4]) for j in jobs])
+    stats = (FalconStats * k)()
+    _check(load().falcon_run_many(k, hs, js, outs, stats))
+    return list(stats)
 
 
 def graph_info(g: Graph):

@@ -176,6 +176,15 @@ struct falcon_graph {
     bool l2_window = false;              // persisting L2 access-policy window on val[]
     cudaAccessPolicyWindow apw = {};
 
+    // ---- views (graph_share): the parent's read-only arrays, own scratch ----
+    falcon_graph *parent = nullptr;       // non-NULL: this handle is a view of `parent`
+    int nviews = 0;                       // (parent) live views
+    // ---- a launched call not yet finished (run_launch / run_finish) ----
+    int pend_algo = -1;
+    uint32_t pend_cap = 0;
+    double pend_relax_ms = -1.0;
+    int64_t pend_relax_launches = 0, pend_cc_passes = 0, pend_cc_launches = 0;
+
     // ---- 1-D vertex partition (multi-GPU) ----
     falcon_comm *comm = nullptr;          // non-NULL: this handle is a partitioned graph
     std::vector<falcon_graph *> parts;    // NCCL: this rank's part; simulated: every part
@@ -488,29 +497,44 @@ void drop_graphs(falcon_graph *g) {
             if (x) { cudaGraphDestroy(x); x = nullptr; }
 }
 
+falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out);
+falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats);
+
+// One call: launch (everything up to the asynchronous copies of the result
+// and the control block) and finish (synchronise, statistics, status).
 falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out, falcon_stats_t *stats) {
     if (g && g->comm) {
         if (style < 0 || style > 3) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
         if (style == DELTA && algo != SSSP) return fail(FALCON_ERR_INVALID_ARG, "FALCON_STYLE_DELTA is an SSSP schedule");
         return run_partitioned(g, algo, source, out, stats);
     }
+    falcon_status_t st = run_launch(g, algo, source, style, out);
+    if (st != FALCON_OK) return st;
+    return run_finish(g, stats);
+}
+
+falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style, int32_t *out) {
+    if (g && g->comm) return fail(FALCON_ERR_UNSUPPORTED, "partitioned graphs run through falcon_sssp/bfs/cc");
+    if (g && g->pend_algo >= 0) return fail(FALCON_ERR_INVALID_ARG, "a call is already in flight on this graph");
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
     if (style < 0 || style > 3) return fail(FALCON_ERR_INVALID_ARG, "unknown style %d", style);
     if (style == DELTA && algo != SSSP) return fail(FALCON_ERR_INVALID_ARG, "FALCON_STYLE_DELTA is an SSSP schedule");
     if (algo != CC && (int64_t)source >= g->n) return fail(FALCON_ERR_INVALID_ARG, "source %u >= n", source);
     CU(cudaSetDevice(g->device));
-    if (style == EDGE) {
-        falcon_status_t st = ensure_src(g);
-        if (st != FALCON_OK) return st;
-    }
-    if (algo == SSSP) {
-        falcon_status_t st = ensure_blocked(g);
-        if (st != FALCON_OK) return st;
-    }
-    if ((algo == BFS && style == VERTEX && g->pull_div) || (algo == CC && style == WORKLIST)) {
-        falcon_status_t st = ensure_reverse(g);
-        if (st != FALCON_OK) return st;
+    if (!g->parent) {   // a view shares layouts its parent built in graph_share
+        if (style == EDGE) {
+            falcon_status_t st = ensure_src(g);
+            if (st != FALCON_OK) return st;
+        }
+        if (algo == SSSP) {
+            falcon_status_t st = ensure_blocked(g);
+            if (st != FALCON_OK) return st;
+        }
+        if ((algo == BFS && style == VERTEX && g->pull_div) || (algo == CC && style == WORKLIST)) {
+            falcon_status_t st = ensure_reverse(g);
+            if (st != FALCON_OK) return st;
+        }
     }
     cudaStream_t s = g->stream;
     Args a = g->args();
@@ -632,22 +656,37 @@ falcon_status_t run(falcon_graph *g, int algo, uint32_t source, int style, int32
     CU(cudaEventRecord(g->ev1, s));
     CU(cudaMemcpyAsync(out, g->val, (size_t)g->n * sizeof(int32_t), cudaMemcpyDefault, s));
     CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
+    g->pend_algo = algo;
+    g->pend_cap = cap;
+    g->pend_relax_ms = relax_ms;
+    g->pend_relax_launches = relax_launches;
+    g->pend_cc_passes = cc_passes;
+    g->pend_cc_launches = cc_launches;
+    return FALCON_OK;
+}
+
+falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats) {
+    if (g->pend_algo < 0) return fail(FALCON_ERR_INVALID_ARG, "no call in flight on this graph");
+    const int algo = g->pend_algo;
+    g->pend_algo = -1;
+    CU(cudaSetDevice(g->device));
+    CU(cudaStreamSynchronize(g->stream));
     const Ctrl &c = *g->h_ctrl;
     if (stats) {
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-        stats->iterations = algo == CC ? cc_passes : c.iter;
+        stats->iterations = algo == CC ? g->pend_cc_passes : c.iter;
         stats->vertices_processed = (int64_t)c.vertices;
         stats->edges_relaxed = (int64_t)c.edges;
         stats->updates = (int64_t)c.updates;
-        stats->kernel_launches = (int64_t)c.launches + cc_launches;
+        stats->kernel_launches = (int64_t)c.launches + g->pend_cc_launches;
         stats->ms = ms;
-        stats->relax_ms = relax_ms;
-        stats->relax_launches = relax_launches;
+        stats->relax_ms = g->pend_relax_ms;
+        stats->relax_launches = g->pend_relax_launches;
     }
     if (c.status == ST_OVERFLOW) return fail(FALCON_ERR_OVERFLOW, "a finite distance would reach FALCON_INF");
-    if (c.status == ST_NOT_CONVERGED) return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", cap);
+    if (c.status == ST_NOT_CONVERGED)
+        return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", g->pend_cap);
     g_last_error.clear();
     return FALCON_OK;
 }
@@ -663,6 +702,12 @@ void destroy(falcon_graph *g) {
     }
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
+    if (g->parent) {   // a view: the arrays below belong to the parent
+        g->parent->nviews--;
+        g->row_off = g->col = g->src = g->rowb = g->srcb = g->rin_off = g->rin_col = g->tiles = nullptr;
+        g->w = nullptr; g->cw = g->cwb = g->chunk = g->chunkb = g->chunks = nullptr;
+        g->d_flags = nullptr;
+    }
     for (auto &row : g->execs)
         for (auto &x : row)
             if (x) cudaGraphExecDestroy(x);
@@ -807,6 +852,57 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     return FALCON_OK;
 }
 
+// graph_share: a view of `p` -- its read-only graph arrays (CSR, COO, chunk
+// ranges, blocked layout, reverse CSR: all built here, once, on the parent)
+// and its own scratch (value array, bitmaps, queues, control block, counters,
+// stream, CUDA graphs), so calls on the parent and on its views may run at
+// the same time (falcon_run_many; the paper's concurrent kernels,
+// PAPER.md:1040-1064).
+falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_graph *v) {
+    CU(cudaSetDevice(p->device));
+    falcon_status_t st = ensure_src(p);
+    if (st == FALCON_OK) st = ensure_blocked(p);
+    if (st == FALCON_OK) st = ensure_reverse(p);
+    if (st != FALCON_OK) return st;
+    v->parent = p;
+    v->device = p->device;
+    v->n = p->n; v->m = p->m;
+    v->row_off = p->row_off; v->col = p->col; v->src = p->src; v->w = p->w; v->cw = p->cw;
+    v->rowb = p->rowb; v->srcb = p->srcb; v->cwb = p->cwb;
+    v->chunk = p->chunk; v->chunkb = p->chunkb; v->chunks = p->chunks;
+    v->nblk = p->nblk; v->bsz = p->bsz; v->blk_bytes = p->blk_bytes;
+    v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq;
+    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div;
+    v->nwords = p->nwords; v->num_sms = p->num_sms;
+    v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
+    v->grid_pull = p->grid_pull; v->grid_cc = p->grid_cc; v->grid_edge = p->grid_edge; v->grid_edge_b = p->grid_edge_b;
+    v->grid_small = p->grid_small; v->cnt_slots = p->cnt_slots;
+    v->delta = p->delta; v->delta_auto = p->delta_auto; v->variant = p->variant;
+    v->persist = p->persist; v->persist_max = p->persist_max;
+    p->nviews++;
+    if (opts && opts->cuda_stream) {
+        v->stream = (cudaStream_t)opts->cuda_stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking));
+        v->own_stream = true;
+    }
+    CU(cudaStreamCreateWithFlags(&v->cap_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&v->ev0));
+    CU(cudaEventCreate(&v->ev1));
+    const size_t n = (size_t)p->n;
+    CU(dmalloc(&v->val, n));
+    CU(dmalloc(&v->bm, 4 * (size_t)v->nwords));
+    CU(dmalloc(&v->fr0, n + 1));
+    CU(dmalloc(&v->fr1, n + 1));
+    CU(dmalloc(&v->ctrl, 1));
+    CU(dmalloc(&v->cnt, 3 * (size_t)v->cnt_slots));
+    CU(cudaMallocHost(&v->h_ctrl, sizeof(Ctrl)));
+    v->l2_window = p->l2_window;
+    v->apw = p->apw;
+    v->apw.base_ptr = v->val;
+    return FALCON_OK;
+}
+
 }  // namespace
 
 #include "partition.cuh"
@@ -838,7 +934,56 @@ falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, co
 }
 
 falcon_status_t graph_free(falcon_graph_t *g) {
+    if (g && g->nviews > 0) return fail(FALCON_ERR_INVALID_ARG, "graph has %d live views (free them first)", g->nviews);
     destroy(g);
+    return FALCON_OK;
+}
+
+falcon_status_t graph_share(falcon_graph_t *g, const falcon_load_opts_t *opts, falcon_graph_t **out) {
+    if (!g || !out) return fail(FALCON_ERR_INVALID_ARG, "graph or out is NULL");
+    *out = nullptr;
+    if (g->comm) return fail(FALCON_ERR_UNSUPPORTED, "graph_share of a partitioned graph");
+    falcon_graph *root = g->parent ? g->parent : g;   // a view of a view shares the root's arrays
+    falcon_graph *v = new (std::nothrow) falcon_graph();
+    if (!v) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    falcon_status_t st = share(root, opts, v);
+    if (st != FALCON_OK) {
+        std::string msg = g_last_error;
+        if (v->parent) destroy(v); else delete v;
+        g_last_error = msg;
+        return st;
+    }
+    g_last_error.clear();
+    *out = v;
+    return FALCON_OK;
+}
+
+falcon_status_t falcon_run_many(int njobs, falcon_graph_t *const *graphs, const falcon_job_t *jobs,
+                                int32_t *const *outs, falcon_stats_t *stats) {
+    if (njobs < 0 || (njobs > 0 && (!graphs || !jobs || !outs))) return fail(FALCON_ERR_INVALID_ARG, "bad job arrays");
+    for (int i = 0; i < njobs; i++) {
+        if (!graphs[i]) return fail(FALCON_ERR_INVALID_ARG, "job %d: graph is NULL", i);
+        if (graphs[i]->comm) return fail(FALCON_ERR_UNSUPPORTED, "job %d: partitioned graph", i);
+        if (jobs[i].algo < FALCON_ALGO_SSSP || jobs[i].algo > FALCON_ALGO_CC)
+            return fail(FALCON_ERR_INVALID_ARG, "job %d: unknown algorithm %d", i, (int)jobs[i].algo);
+        for (int j = 0; j < i; j++)
+            if (graphs[j] == graphs[i])
+                return fail(FALCON_ERR_INVALID_ARG, "jobs %d and %d share a graph handle (use graph_share)", j, i);
+    }
+    int launched = 0;
+    falcon_status_t first = FALCON_OK;
+    std::string msg;
+    for (; launched < njobs; launched++) {   // every job is in flight before any is waited on
+        const falcon_job_t &J = jobs[launched];
+        falcon_status_t st = run_launch(graphs[launched], (int)J.algo, J.source, (int)J.style, outs[launched]);
+        if (st != FALCON_OK) { first = st; msg = g_last_error; break; }
+    }
+    for (int i = 0; i < launched; i++) {
+        falcon_status_t st = run_finish(graphs[i], stats ? stats + i : nullptr);
+        if (st != FALCON_OK && first == FALCON_OK) { first = st; msg = g_last_error; }
+    }
+    if (first != FALCON_OK) { g_last_error = msg; return first; }
+    g_last_error.clear();
     return FALCON_OK;
 }
 
@@ -937,6 +1082,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
     if (g->comm) targets = g->parts; else targets.push_back(g);
     for (falcon_graph *t : targets) {
         if (!strcmp(name, "block_bytes")) {
+            if (t->parent || t->nviews)
+                return fail(FALCON_ERR_UNSUPPORTED, "block_bytes of a graph shared with views (the layout is shared)");
             if (t->stream) cudaStreamSynchronize(t->stream);
             dfree(t->rowb); dfree(t->cwb); dfree(t->srcb); dfree(t->chunkb);
             t->rowb = nullptr; t->cwb = nullptr; t->srcb = nullptr; t->chunkb = nullptr; t->nblk = 1; t->bsz = 0;

@@ -1,8 +1,4 @@
-cp paper_1903_01665_b200/libfalcon.so /tmp/libfalcon_pf.so
-for V in pf nopf; do
-cp /tmp/libfalcon_pf.so paper_1903_01665_b200/libfalcon.so
-[ $V = nopf ] && cp paper_1903_01665_b200/libfalcon_nopf.so paper_1903_01665_b200/libfalcon.so
-timeout 600 python tools/survey.py --algos sssp,bfs --styles edge --reps 3 2>&1 | grep -v "==" | sed "s/^/$V /"
-done
-cp /tmp/libfalcon_pf.so paper_1903_01665_b200/libfalcon.so
-timeout 900 python -m pytest tests -m gpu -x -q -k "not full_config and not three_passes" 2>&1 | tail -1
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -k "not full_config" > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
+timeout 900 python tools/concurrency.py --configs rand-25M,rmat-10M,grid-24M --reps 3 > gpurun_out/concurrency.log 2>&1
+timeout 600 python tools/survey.py --configs rand-25M --reps 3 > gpurun_out/survey.log 2>&1
