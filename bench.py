@@ -50,9 +50,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-max-steps", type=int, default=3)
-    ap.add_argument("--mode", default="replica", choices=["replica", "partition"],
-                    help="N>1: replica = one independent graph per GPU (PAPER.md:1587-1597 'parallel "
-                         "sections', weak scaling); partition = one graph 1-D vertex-partitioned over the "
+    ap.add_argument("--mode", default="replica", choices=["replica", "sections", "partition"],
+                    help="N>1: replica = one independent graph per GPU (weak scaling); sections = the same "
+                         "graph on every GPU, the step's (algo, style) runs dealt round-robin to the GPUs "
+                         "(PAPER.md:1587-1597 'parallel sections', SURVEY §8(f) row 2; strong scaling, "
+                         "time = max over GPUs); partition = one graph 1-D vertex-partitioned over the "
                          "GPUs with NCCL exchange (SURVEY.md §8(e), strong scaling)")
     ap.add_argument("--simulate", type=int, default=0,
                     help="partition mode on ONE GPU with this many simulated parts (device-side exchange)")
@@ -260,7 +262,8 @@ def main():
     partition = args.mode == "partition" or args.simulate > 0
     # Workload: the BASELINE.json config; replica r uses seed + r (weak scaling);
     # partition mode: the same graph on every rank (each keeps its rows).
-    if world > 1 and rank > 0 and not partition:
+    sections = args.mode == "sections" and not partition
+    if world > 1 and rank > 0 and not partition and not sections:
         base = gg.CONFIGS[args.config]
         G = {"rand-25M": lambda: gg.er(25_000_000, 100_000_000, 25 + rank, name="rand-25M"),
              "rmat-10M": lambda: gg.rmat(10_000_000, 100_000_000, 10 + rank, name="rmat-10M"),
@@ -281,7 +284,8 @@ def main():
     g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream,
                           flags=0 if partition else fb.LOAD_BUILD_COO, comm=comm)
     out = torch.empty(G.n, dtype=torch.int32, device="cuda")
-    runs = [(a, s) for a in algos for s in styles if s != "delta" or a == "sssp"]   # DELTA is SSSP-only
+    all_runs = [(a, s) for a in algos for s in styles if s != "delta" or a == "sssp"]   # DELTA is SSSP-only
+    runs = all_runs[rank::world] if sections else all_runs   # parallel sections: this GPU's share
 
     def step(collect=None):
         launches = 0
@@ -297,7 +301,7 @@ def main():
     for a in algos:
         fb.run(g, a, styles[0], out, G.source)
         mc[a] = m_counted(G, a, out.cpu().numpy())
-    units_per_step = sum(mc[a] for a, _ in runs)
+    units_per_step = sum(mc[a] for a, _ in (all_runs if sections else runs))   # sections: all GPUs' runs
 
     for _ in range(args.warmup):
         step()
@@ -323,14 +327,15 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    replicas = world if not partition else 1   # partition: one shared graph (strong scaling)
+    replicas = world if not (partition or sections) else 1   # partition / sections: one job (strong scaling)
     value = replicas * units_per_step * args.steps / (ms_total * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel: one profiled step (host-driven loop,
     # CUDA events around every relax launch on the library stream)
     hbm, hbm_src = peaks()
     prof = {}
-    if not partition:
+    roofline = None
+    if not partition and runs:
         fb.falcon_set_profiling(g, True)
         step(prof)
         fb.falcon_set_profiling(g, False)
@@ -354,7 +359,7 @@ def main():
                                   "peak_source": "profiles/l2_peaks.json (tools/l2probe3.cu)"}
         except (OSError, KeyError, ValueError):
             pass
-    else:   # partitioned: the whole superstep loop (relax + exchange) of the slowest algorithm
+    elif partition:   # partitioned: the whole superstep loop (relax + exchange) of the slowest algorithm
         worst = max(per_run, key=lambda k: statistics.median(x["ms"] for x in per_run[k]))
         x = per_run[worst][-1]
         ms = statistics.median(y["ms"] for y in per_run[worst])
@@ -407,7 +412,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": replicas * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",
-               "h2d_bytes_per_step": 4 * (G.n + 1) + 8 * G.m, "d2h_bytes_per_step": 4 * G.n * len(runs),
+               "h2d_bytes_per_step": 4 * (G.n + 1) + 8 * G.m, "d2h_bytes_per_step": 4 * G.n * len(all_runs),
                "steps": e_steps, "ms_per_step": ems / e_steps}
 
     cpu = None
@@ -420,13 +425,15 @@ def main():
     if rank == 0:
         line = {"metric": "SSSP/BFS/CC GTEPS (aggregate over runs per step)", "value": value, "unit": "GTEPS",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "strong" if partition else "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong" if (partition or sections) else "weak",
+                "vs_baseline": None,
                 "dtype": "int32", "data": "synthetic",
                 "config": {"workload": args.config, "n": G.n, "m": G.m, "source": G.source, "algos": algos,
-                           "styles": styles, "runs_per_step": len(runs),
+                           "styles": styles, "runs_per_step": len(all_runs),
                            "parallelism": (f"partition{world}" + (f" (simulated {args.simulate} parts on 1 GPU)"
                                                                    if args.simulate else "")) if partition
-                           else ("replicas" if world > 1 else "single"),
+                           else (f"sections{world}" if sections and world > 1
+                                 else ("replicas" if world > 1 else "single")),
                            "l2": "inputs larger than L2 (CSR+COO %.2f GB vs 126 MB L2); each run re-initialises "
                                  "its value array" % ((4 * (G.n + 1) + 12 * G.m) / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
