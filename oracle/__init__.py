@@ -59,7 +59,9 @@ def _L():
         lib.oracle_sssp.argtypes = [ctypes.c_int64, p, p, p, ctypes.c_uint32, p]
         lib.oracle_bfs.argtypes = [ctypes.c_int64, p, p, ctypes.c_uint32, p]
         lib.oracle_cc.argtypes = [ctypes.c_int64, p, p, p]
-        for f in (lib.oracle_sssp, lib.oracle_bfs, lib.oracle_cc):
+        lib.oracle_mst.argtypes = [ctypes.c_int64, p, p, p, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_int64), p]
+        for f in (lib.oracle_sssp, lib.oracle_bfs, lib.oracle_cc, lib.oracle_mst):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -105,6 +107,20 @@ def cc(row_off, col) -> np.ndarray:
     if rc:
         raise OracleError(_ERR.get(rc, str(rc)))
     return out
+
+
+def mst(row_off, col, w=None):
+    """Minimum spanning forest of the undirected view (Kruskal): returns
+    (total weight, number of forest edges, min-id tree label per vertex)."""
+    row_off = _c(row_off, np.uint32); col = _c(col, np.uint32)
+    w = None if w is None else _c(w, np.int32)
+    n = len(row_off) - 1
+    label = np.empty(n, np.int32)
+    tot, ne = ctypes.c_int64(), ctypes.c_int64()
+    rc = _L().oracle_mst(n, _p(row_off), _p(col), _p(w), ctypes.byref(tot), ctypes.byref(ne), _p(label))
+    if rc:
+        raise OracleError(_ERR.get(rc, str(rc)))
+    return tot.value, ne.value, label
 
 
 def run(algo: str, g) -> np.ndarray:

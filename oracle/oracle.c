@@ -20,6 +20,8 @@
  *   oracle_cc   : union-find over all arcs (weak components), label = minimum
  *                 vertex id in the component (SPEC.md:452 min-label
  *                 convention; reading R6).
+ *   oracle_mst  : Kruskal over the undirected view -> total weight of a
+ *                 minimum spanning forest (§8(f) row 4).
  *
  * Conventions (DESIGN.md §2 readings): INF = 2147483647 = MAX_INT
  * (PAPER.md:1679); weights must be >= 0; a finite
@@ -165,5 +167,71 @@ int oracle_cc(int64_t n, const uint32_t *row_off, const uint32_t *col, int32_t *
         label[v] = (int32_t)minid[r];
     }
     free(parent); free(size); free(minid);
+    return 0;
+}
+
+/* ---------------- minimum spanning forest ----------------
+ * The paper's fourth algorithm ("Minimum Spanning Tree computation
+ * (MST)", Table 2 MST column); "MST total weight == Kruskal
+ * oracle".  Every arc u->v is the undirected edge {u, v} (the graph is a
+ * directed multigraph; SPEC.md:571 duplicates tolerated), so the result is a
+ * minimum spanning forest: one minimum spanning tree per weak component.
+ * Kruskal (1956): arcs in ascending weight order (ties by arc index), an arc
+ * joins the forest iff its endpoints lie in different trees (union-find).
+ *   *total  = sum of the weights of the joined arcs -- the same for every
+ *             minimum spanning forest, whatever the order among equal weights;
+ *   *nedges = number of joined arcs = n - #components;
+ *   label   = (nullable) min vertex id of the tree (= the CC label).
+ * w == NULL means every weight is 1.  Returns 0 ok, 1 bad argument / negative
+ * weight, 3 OOM. */
+static const int32_t *g_mst_w;
+static int mst_cmp(const void *a, const void *b) {
+    const uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    const int32_t wx = g_mst_w ? g_mst_w[x] : 1, wy = g_mst_w ? g_mst_w[y] : 1;
+    if (wx != wy) return wx < wy ? -1 : 1;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+int oracle_mst(int64_t n, const uint32_t *row_off, const uint32_t *col, const int32_t *w, int64_t *total,
+               int64_t *nedges, int32_t *label) {
+    if (n < 0 || !row_off || !total || !nedges) return 1;
+    *total = 0; *nedges = 0;
+    if (n == 0) return 0;
+    const uint64_t m = row_off[n];
+    if (w)
+        for (uint64_t e = 0; e < m; e++)
+            if (w[e] < 0) return 1;
+    uint32_t *src = (uint32_t *)malloc((m ? m : 1) * sizeof(uint32_t));
+    uint32_t *order = (uint32_t *)malloc((m ? m : 1) * sizeof(uint32_t));
+    uint32_t *parent = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t *size = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    int64_t *minid = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    if (!src || !order || !parent || !size || !minid) {
+        free(src); free(order); free(parent); free(size); free(minid);
+        return 3;
+    }
+    for (int64_t u = 0; u < n; u++)
+        for (uint32_t e = row_off[u]; e < row_off[u + 1]; e++) src[e] = (uint32_t)u;
+    for (uint64_t e = 0; e < m; e++) order[e] = (uint32_t)e;
+    g_mst_w = w;
+    qsort(order, m, sizeof(uint32_t), mst_cmp);
+    for (int64_t v = 0; v < n; v++) { parent[v] = (uint32_t)v; size[v] = 1; minid[v] = -1; }
+    for (uint64_t i = 0; i < m; i++) {
+        const uint32_t e = order[i];
+        uint32_t a = uf_find(parent, src[e]), b = uf_find(parent, col[e]);
+        if (a == b) continue;                      /* would close a cycle (or a self loop) */
+        if (size[a] < size[b]) { uint32_t t = a; a = b; b = t; }
+        parent[b] = a; size[a] += size[b];
+        *total += w ? w[e] : 1;
+        *nedges += 1;
+    }
+    if (label) {
+        for (int64_t v = 0; v < n; v++) {
+            uint32_t r = uf_find(parent, (uint32_t)v);
+            if (minid[r] < 0) minid[r] = v;
+            label[v] = (int32_t)minid[r];
+        }
+    }
+    free(src); free(order); free(parent); free(size); free(minid);
     return 0;
 }

@@ -32,6 +32,10 @@ def test_golden(fname):
         assert np.array_equal(oracle.bfs(row_off, col, g.source), g.expect["bfs"])
     if "cc" in g.expect:
         assert np.array_equal(oracle.cc(row_off, col), g.expect["cc"])
+    if "mst" in g.expect:
+        tot, ne, lab = oracle.mst(row_off, col, w)
+        assert [tot, ne] == g.expect["mst"].tolist()
+        assert np.array_equal(lab, oracle.cc(row_off, col))
 
 
 # ------------------------------------------------------------------ brute force
@@ -202,3 +206,114 @@ def test_certificates_reject_plausible_mistakes():
     if not np.array_equal(bad, lab):
         with pytest.raises(AssertionError):
             cert_cc(g.row_off, g.col, bad, ncomp)
+
+
+# ------------------------------------------------------------------ MST
+def _msf_brute(n, src, dst, w):
+    """Minimum spanning forest weight by exhaustive search over arc subsets
+    (tiny graphs only): the lightest acyclic subset with n - #components arcs."""
+    import itertools
+    src = [int(x) for x in src]; dst = [int(x) for x in dst]; w = [int(x) for x in w]
+    comps = len(set(closure_cc(n, src, dst).tolist())) if n else 0
+    k = n - comps
+    best = None
+    for sub in itertools.combinations(range(len(src)), k):
+        par = list(range(n))
+
+        def f(x):
+            while par[x] != x:
+                x = par[x]
+            return x
+        ok = True
+        for e in sub:
+            a, b = f(src[e]), f(dst[e])
+            if a == b:
+                ok = False
+                break
+            par[a] = b
+        if ok:
+            tot = sum(w[e] for e in sub)
+            best = tot if best is None or tot < best else best
+    return (best if best is not None else 0), k
+
+
+def _msf_prim(n, src, dst, w):
+    """Prim's algorithm (dense O(n^2)) per component on the symmetrised,
+    min-combined adjacency -- a different textbook algorithm than Kruskal."""
+    big = np.iinfo(np.int64).max
+    A = np.full((n, n), big, dtype=np.int64)
+    for u, v, x in zip(np.asarray(src, np.int64), np.asarray(dst, np.int64), np.asarray(w, np.int64)):
+        if u != v and x < A[u, v]:
+            A[u, v] = A[v, u] = x
+    done = np.zeros(n, bool)
+    tot = edges = 0
+    for r in range(n):
+        if done[r]:
+            continue
+        key = A[r].copy()
+        done[r] = True
+        while True:
+            cand = np.where(~done & (key < big))[0]
+            if len(cand) == 0:
+                break
+            v = cand[np.argmin(key[cand])]
+            tot += int(key[v]); edges += 1
+            done[v] = True
+            key = np.minimum(key, A[v])
+    return tot, edges
+
+
+@pytest.mark.parametrize("case", range(0, 220, 1))
+def test_mst_tiny_prim_and_brute(case):
+    n, src, dst, w, _ = _tiny_graphs()[case]
+    row_off, col, wc = gg.csr_from_edges(n, src, dst, w)
+    tot, ne, lab = oracle.mst(row_off, col, wc)
+    assert (tot, ne) == _msf_prim(n, src, dst, w)
+    assert np.array_equal(lab, oracle.cc(row_off, col))
+    if len(src) <= 12 and n <= 9:
+        assert (tot, ne) == _msf_brute(n, src, dst, w)
+
+
+def test_mst_brute_many_tiny():
+    rng = np.random.default_rng(470)
+    for _ in range(300):
+        n = int(rng.integers(1, 8)); m = int(rng.integers(0, 11))
+        src = rng.integers(0, n, m).astype(np.uint32); dst = rng.integers(0, n, m).astype(np.uint32)
+        w = rng.integers(0, 5, m).astype(np.int32)   # many ties and zeros
+        row_off, col, wc = gg.csr_from_edges(n, src, dst, w)
+        tot, ne, _ = oracle.mst(row_off, col, wc)
+        assert (tot, ne) == _msf_brute(n, src, dst, w)
+
+
+@pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s"])
+def test_mst_scipy_medium(name):
+    """scipy.sparse.csgraph.minimum_spanning_tree on the symmetrised graph with
+    min-combined duplicates (weights >= 1 here: scipy drops zero entries)."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import minimum_spanning_tree
+    G = gg.config(name)
+    src = np.repeat(np.arange(G.n), np.diff(G.row_off.astype(np.int64)))
+    dst = G.col.astype(np.int64); w = G.w.astype(np.int64)
+    keep = src != dst
+    a = np.minimum(src, dst)[keep]; b = np.maximum(src, dst)[keep]; w = w[keep]
+    key = a * G.n + b
+    order = np.lexsort((w, key))
+    key, w = key[order], w[order]
+    first = np.r_[True, key[1:] != key[:-1]]
+    key, w = key[first], w[first]          # min weight per undirected pair
+    M = sp.csr_matrix((w.astype(np.float64), (key // G.n, key % G.n)), shape=(G.n, G.n))
+    T = minimum_spanning_tree(M)
+    tot, ne, lab = oracle.mst(G.row_off, G.col, G.w)
+    assert tot == int(round(T.sum())) and ne == T.nnz
+    assert np.array_equal(lab, oracle.cc(G.row_off, G.col))
+
+
+def test_mst_unit_weights_and_special_cases():
+    G = gg.config("rmat-s")
+    tot, ne, lab = oracle.mst(G.row_off, G.col, None)   # all weights 1
+    comps = len(np.unique(oracle.cc(G.row_off, G.col)))
+    assert tot == ne == G.n - comps
+    ro = np.zeros(6, np.uint32)                          # no arcs: every vertex its own tree
+    assert oracle.mst(ro, np.zeros(0, np.uint32), np.zeros(0, np.int32))[:2] == (0, 0)
+    with pytest.raises(oracle.OracleError):
+        oracle.mst(np.array([0, 1], np.uint32), np.array([0], np.uint32), np.array([-1], np.int32))
