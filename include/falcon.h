@@ -201,6 +201,21 @@ FALCON_API falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon
  * label_out: (host|device) int32[n]. */
 FALCON_API falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats);
 
+/* Minimum spanning forest of the undirected view (every arc u->v is the edge
+ * {u, v}; self loops never join, duplicates allowed): *total_weight = the
+ * total weight of a minimum spanning tree of every weak component -- the
+ * paper's MST (Table 2), checked against Kruskal (SPEC.md:470,
+ * 492).  Borůvka rounds: per round every component picks its
+ * lightest incident arc (ties by arc index), components hook across their
+ * picks, pointer jumping flattens; at most log2(n) + 1 rounds.
+ * forest_edges (nullable) = number of forest edges = n - #components;
+ * label_out (nullable, host|device int32[n]) = min vertex id of the vertex's
+ * tree (= the CC label).  style: VERTEX (CSR rows) or EDGE (COO arcs).
+ * Errors: INVALID_ARG (NULL g / total_weight), UNSUPPORTED (other styles,
+ * partitioned graph), CUDA. */
+FALCON_API falcon_status_t falcon_mst(falcon_graph_t *g, falcon_style_t style, int64_t *total_weight,
+                                      int64_t *forest_edges, int32_t *label_out, falcon_stats_t *stats);
+
 /* Bucket width Δ of FALCON_STYLE_DELTA (SSSP): vertices with tentative
  * distance < T are relaxed from the near queue, the others wait in a far set
  * until the near queue is empty and T advances to the next non-empty bucket.

@@ -6,7 +6,7 @@ every call raises.  Arrays may be numpy arrays (host) or torch tensors (host
 or CUDA); PyTorch is used only for device memory and streams.
 
 Names follow the C ABI: graph_load_csr, graph_free, graph_info, graph_owned_range,
-graph_share, falcon_run_many, falcon_sssp, falcon_bfs, falcon_cc, falcon_set_profiling, falcon_set_delta, falcon_set_option,
+graph_share, falcon_run_many, falcon_sssp, falcon_bfs, falcon_cc, falcon_mst, falcon_set_profiling, falcon_set_delta, falcon_set_option,
 falcon_partition, falcon_comm_unique_id, falcon_comm_init,
 falcon_comm_init_simulated, falcon_comm_free, falcon_last_error, falcon_version.
 """
@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "graph_share", "falcon_run_many", "falcon_sssp", "falcon_bfs", "falcon_cc",
+__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "graph_share", "falcon_run_many", "falcon_mst", "falcon_sssp", "falcon_bfs", "falcon_cc",
            "falcon_set_profiling", "falcon_set_delta", "falcon_set_option", "falcon_partition", "falcon_comm_unique_id",
            "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_free", "graph_owned_range", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
@@ -89,6 +89,9 @@ def load(build_if_missing: bool = False):
     lib.falcon_comm_init_simulated.argtypes = [ctypes.c_int, ctypes.POINTER(p)]
     lib.falcon_comm_free.argtypes = [p]
     lib.graph_owned_range.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.falcon_mst.argtypes = [p, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64), p,
+                               ctypes.POINTER(FalconStats)]
+    lib.falcon_mst.restype = st
     lib.graph_share.argtypes = [p, ctypes.POINTER(_LoadOpts), ctypes.POINTER(p)]
     lib.graph_share.restype = st
     lib.falcon_run_many.argtypes = [ctypes.c_int, ctypes.POINTER(p), ctypes.POINTER(_Job), ctypes.POINTER(p),
@@ -296,6 +299,18 @@ def falcon_cc(g: Graph, style, label_out) -> FalconStats:
     _check_dtype(label_out, "i32", "label_out")
     _check(load().falcon_cc(g.handle, _style(style), _ptr(label_out), ctypes.byref(st)))
     return st
+
+
+def falcon_mst(g: Graph, style, label_out=None):
+    """Minimum spanning forest: returns (total weight, forest edges, FalconStats);
+    label_out (optional int32[n]) receives the min-id tree label per vertex."""
+    st = FalconStats()
+    if label_out is not None:
+        _check_dtype(label_out, "i32", "label_out")
+    tot, ne = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().falcon_mst(g.handle, _style(style), ctypes.byref(tot), ctypes.byref(ne), _ptr(label_out),
+                             ctypes.byref(st)))
+    return tot.value, ne.value, st
 
 
 def falcon_set_profiling(g: Graph, enable: bool):

@@ -26,6 +26,7 @@
 #include "../../include/falcon.h"
 #include "kernels.cuh"
 #include "cc.cuh"
+#include "mst.cuh"
 
 using namespace fk;
 
@@ -176,6 +177,9 @@ struct falcon_graph {
     bool l2_window = false;              // persisting L2 access-policy window on val[]
     cudaAccessPolicyWindow apw = {};
 
+    unsigned long long *mst_best = nullptr;   // MST: per-component best arc key, built lazily
+    uint32_t *mst_list = nullptr;             // MST: two live lists (arcs or vertices) of mst_lcap entries
+    size_t mst_lcap = 0;
     // ---- views (graph_share): the parent's read-only arrays, own scratch ----
     falcon_graph *parent = nullptr;       // non-NULL: this handle is a view of `parent`
     int nviews = 0;                       // (parent) live views
@@ -691,6 +695,90 @@ falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats) {
     return FALCON_OK;
 }
 
+// Minimum spanning forest (mst.cuh): Borůvka rounds, each checked on the
+// host (at most log2(n) + 1 rounds).
+falcon_status_t run_mst(falcon_graph *g, int style, int64_t *total, int64_t *nedges, int32_t *label_out,
+                        falcon_stats_t *stats) {
+    if (!g || !total) return fail(FALCON_ERR_INVALID_ARG, "graph or total is NULL");
+    if (g->comm) return fail(FALCON_ERR_UNSUPPORTED, "falcon_mst on a partitioned graph");
+    if (style != VERTEX && style != EDGE)
+        return fail(FALCON_ERR_UNSUPPORTED, "falcon_mst runs VERTEX or EDGE style (Borůvka is arc-parallel)");
+    if (g->pend_algo >= 0) return fail(FALCON_ERR_INVALID_ARG, "a call is already in flight on this graph");
+    CU(cudaSetDevice(g->device));
+    if (!g->parent) {
+        falcon_status_t st = ensure_src(g);
+        if (st != FALCON_OK) return st;
+    }
+    if (!g->mst_best) CU(dmalloc(&g->mst_best, (size_t)g->n));
+    // live lists (EDGE: arc indices, VERTEX: vertices), ping-pong
+    const size_t lcap = (size_t)(style == EDGE ? g->m : g->n) + 1;
+    if (g->mst_lcap < lcap) {
+        dfree(g->mst_list);
+        g->mst_list = nullptr;
+        CU(dmalloc(&g->mst_list, 2 * lcap));
+        g->mst_lcap = lcap;
+    }
+    cudaStream_t s = g->stream;
+    Args a = g->args();
+    const int gs = g->grid_small;
+    CU(cudaEventRecord(g->ev0, s));
+    k_init<CC><<<gs, BLOCK, 0, s>>>(a, 0, 64, 3u * g->cnt_slots, VERTEX, 1);   // comp[v] = v
+    int64_t rounds = 0, launches = 2, hooks = 0;
+    const uint32_t *in = nullptr;   // first round: every vertex / arc
+    uint32_t nin = 0;
+    bool collect = false;           // write this round's live list (else only count it)
+    for (;;) {
+        uint32_t *out = collect ? g->mst_list + (rounds & 1) * g->mst_lcap : nullptr;
+        k_mst_reset<<<gs, BLOCK, 0, s>>>(a, g->mst_best);
+        if (style == VERTEX) k_mst_min_vertex<BLOCK><<<g->grid_cc, BLOCK, 0, s>>>(a, g->mst_best, in, nin, out);
+        else k_mst_min_edge<BLOCK><<<gs, BLOCK, 0, s>>>(a, g->mst_best, in, nin, out);
+        k_mst_hook<BLOCK><<<gs, BLOCK, 0, s>>>(a, g->mst_best, g->fr0);
+        k_mst_apply<<<gs, BLOCK, 0, s>>>(a, g->fr0);
+        launch_l2(g, k_compress, gs, s, a);
+        launches += 5;
+        rounds++;
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        hooks += g->h_ctrl->hooks;
+        if (g->h_ctrl->hooks == 0) break;
+        if (rounds > 64) return fail(FALCON_ERR_NOT_CONVERGED, "Borůvka did not converge in 64 rounds");
+        // the live list replaces a full scan once it is short (indirect
+        // gathers cost more than streaming while most arcs are still live)
+        nin = g->h_ctrl->found;   // live items of this round (the list holds them if collected)
+        in = out && (uint64_t)nin * 4 < lcap ? out : nullptr;
+        collect = (uint64_t)nin * 2 < lcap;
+    }
+    uint32_t *minid = reinterpret_cast<uint32_t *>(g->mst_best);
+    CU(cudaMemsetAsync(minid, 0xff, (size_t)g->n * 4, s));
+    k_mst_minid<<<gs, BLOCK, 0, s>>>(a, minid);
+    k_mst_label<<<gs, BLOCK, 0, s>>>(a, minid);
+    k_finish<<<1, BLOCK, 0, s>>>(a, (uint32_t)g->cnt_slots);
+    launches += 3;
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(g->ev1, s));
+    if (label_out) CU(cudaMemcpyAsync(label_out, g->val, (size_t)g->n * sizeof(int32_t), cudaMemcpyDefault, s));
+    CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const Ctrl &c = *g->h_ctrl;
+    *total = (int64_t)c.wsum;
+    if (nedges) *nedges = hooks;
+    if (stats) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        stats->iterations = rounds;
+        stats->vertices_processed = (int64_t)g->n * rounds;
+        stats->edges_relaxed = (int64_t)c.edges;
+        stats->updates = hooks;
+        stats->kernel_launches = launches;
+        stats->ms = ms;
+        stats->relax_ms = -1.0;
+        stats->relax_launches = 0;
+    }
+    g_last_error.clear();
+    return FALCON_OK;
+}
+
 void destroy_partitioned(falcon_graph *g);
 
 void destroy(falcon_graph *g) {
@@ -721,7 +809,7 @@ void destroy(falcon_graph *g) {
                     (void *)g->rin_off, (void *)g->rin_col, (void *)g->rowb, (void *)g->cwb, (void *)g->srcb,
                     (void *)g->chunk, (void *)g->chunkb, (void *)g->chunks, (void *)g->val, (void *)g->bm,
                     (void *)g->fr0, (void *)g->fr1, (void *)g->tiles, (void *)g->ctrl, (void *)g->cnt,
-                    (void *)g->d_flags})
+                    (void *)g->d_flags, (void *)g->mst_best, (void *)g->mst_list})
         dfree(p);   // back to the device cache (the stream was synchronised above)
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -1066,6 +1154,11 @@ falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon_style_t st
 
 falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats) {
     return run(g, CC, 0, (int)style, label_out, stats);
+}
+
+falcon_status_t falcon_mst(falcon_graph_t *g, falcon_style_t style, int64_t *total_weight, int64_t *forest_edges,
+                           int32_t *label_out, falcon_stats_t *stats) {
+    return run_mst(g, (int)style, total_weight, forest_edges, label_out, stats);
 }
 
 falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta) {

@@ -64,6 +64,9 @@ struct Ctrl {
     uint32_t blk;         // this round expands over the destination-blocked layout (dense rounds)
     uint32_t noq;         // WORKLIST: this (dense) round marks the bitmap only -- no queue is built
     uint32_t prevnoq;     // WORKLIST: the previous round did: read this round's items from the bitmap
+    uint32_t hooks;       // MST: components hooked this round
+    uint32_t pad_;
+    unsigned long long wsum;       // MST: total weight of the forest edges chosen so far
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
     unsigned long long edges;
@@ -257,7 +260,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
         c->pull = 0; c->found = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
-        c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0;
+        c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
 }

@@ -39,10 +39,14 @@ for cfg in a.configs.split(","):
         for style in a.styles.split(","):
             if style == "delta" and algo != "sssp":
                 continue
-            fb.run(g, algo, style, out, G.source)
+            if algo == "mst" and style not in ("vertex", "edge"):
+                continue
+            one = (lambda: fb.falcon_mst(g, style, out)[2]) if algo == "mst" else \
+                (lambda: fb.run(g, algo, style, out, G.source))
+            one()
             ms = []
             for _ in range(a.reps):
-                st = fb.run(g, algo, style, out, G.source)
+                st = one()
                 ms.append(st.ms)
             print(f"{cfg:9s} {algo:4s} {style:8s} med {statistics.median(ms):8.3f} ms  min {min(ms):8.3f}  "
                   f"iters {st.iterations:6d}  edges {st.edges_relaxed / G.m:6.2f} m  upd {st.updates:11d}  "
