@@ -111,12 +111,20 @@ __device__ __forceinline__ uint32_t *bm_of(const Args &a, uint32_t r) {
 // ------------------------------------------------------------------ loads with L2 policies
 __device__ __forceinline__ uint64_t pol_evict_first() {
     uint64_t p;
+#ifdef FK_NO_EVICT_FIRST
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#else
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
     return p;
 }
 __device__ __forceinline__ uint64_t pol_evict_last() {
     uint64_t p;
+#ifdef FK_NO_EVICT_LAST
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#else
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
     return p;
 }
 // read-only, streamed once per round: no L1 allocation, evict-first in L2

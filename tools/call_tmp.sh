@@ -1,3 +1,6 @@
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 1500 python -m pytest tests/test_mst_gpu.py -x -q > gpurun_out/mst_tests.log 2>&1; echo "rc=$?" >> gpurun_out/mst_tests.log
-timeout 900 python tools/survey.py --algos mst --styles vertex,edge --reps 3 > gpurun_out/survey_mst.log 2>&1
+cp paper_1903_01665_b200/libfalcon.so /tmp/libfalcon_base.so
+for V in base NO_EVICT_LAST NO_EVICT_FIRST; do
+if [ $V = base ]; then cp /tmp/libfalcon_base.so paper_1903_01665_b200/libfalcon.so; else cp paper_1903_01665_b200/libfalcon_$V.so paper_1903_01665_b200/libfalcon.so; fi
+timeout 600 python tools/survey.py --configs rand-25M,rmat-10M --algos sssp,bfs,cc --styles vertex,edge,worklist --reps 3 2>&1 | grep -v "==" | sed "s/^/$V /"
+done > gpurun_out/evict.log
+cp /tmp/libfalcon_base.so paper_1903_01665_b200/libfalcon.so
