@@ -228,7 +228,7 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *   "block_bytes"  value-array bytes per destination block of the SSSP arc
  *                  layout (default 64 MiB, env FALCON_BLOCK_MB; 0 = no blocking)
  *   "dense_div"    a round is dense (bitmap-driven, items in vertex order)
- *                  when its frontier exceeds n / dense_div (default 16,
+ *                  when its frontier exceeds n / dense_div (default 32,
  *                  env FALCON_DENSE_DIV; 0 = never)
  *   "block_div"    an SSSP round walks the blocked layout when its frontier
  *                  exceeds n / block_div (default 8, env FALCON_BLOCK_DIV;

@@ -149,7 +149,7 @@ struct falcon_graph {
     uint2 *chunks = nullptr;                     // ... of src in SSSP chunks (unblocked graphs)
     uint32_t nblk = 1, bsz = 0;
     size_t blk_bytes = 64u << 20;        // value-array bytes per block (FALCON_BLOCK_MB)
-    uint32_t dense_div = 16;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV)
+    uint32_t dense_div = 32;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV; swept 8-128)
     uint32_t blk_div = 8;                // blocked round: frontier > n / blk_div (FALCON_BLOCK_DIV)
     uint32_t wl_noq = 1;                 // WORKLIST dense rounds without claims / queue (FALCON_WL_NOQ)
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily

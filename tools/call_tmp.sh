@@ -1,6 +1,4 @@
-cp paper_1903_01665_b200/libfalcon.so /tmp/libfalcon_base.so
-for V in base NO_EVICT_LAST NO_EVICT_FIRST; do
-if [ $V = base ]; then cp /tmp/libfalcon_base.so paper_1903_01665_b200/libfalcon.so; else cp paper_1903_01665_b200/libfalcon_$V.so paper_1903_01665_b200/libfalcon.so; fi
-timeout 600 python tools/survey.py --configs rand-25M,rmat-10M --algos sssp,bfs,cc --styles vertex,edge,worklist --reps 3 2>&1 | grep -v "==" | sed "s/^/$V /"
-done > gpurun_out/evict.log
-cp /tmp/libfalcon_base.so paper_1903_01665_b200/libfalcon.so
+run() { timeout 600 python tools/survey.py --configs $4 --algos $1 --styles $2 --reps 3 2>&1 | grep -v "==" | sed "s/^/$3 /"; }
+for D in 16 32 64 128; do
+FALCON_DENSE_DIV=$D run sssp,bfs worklist dense$D rand-25M,rmat-10M,grid-24M
+done
