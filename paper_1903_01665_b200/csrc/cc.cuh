@@ -53,7 +53,8 @@ __device__ __forceinline__ bool uf_unite(int32_t *L, uint32_t a, uint32_t b) {
 
 // VERTEX: warp-cooperative walk over all vertices' out-arcs (same shuffle
 // scan / binary search as k_expand_warp), unite(u, v) per arc.
-template <int B>
+// MAXD > 0: only the first MAXD arcs of every row (WORKLIST sampling, R15).
+template <int B, int MAXD = 0>
 __global__ void __launch_bounds__(B) k_cc_vertex(Args a) {
     if (a.ctrl->done) return;
     const int lane = threadIdx.x & 31;
@@ -63,7 +64,12 @@ __global__ void __launch_bounds__(B) k_cc_vertex(Args a) {
     for (uint32_t wb = gw * 32; wb < a.n; wb += nwarps * 32) {
         const uint32_t u = wb + lane;
         uint32_t beg = 0, deg = 0;
-        if (u < a.n) { beg = ld_ro(a.row_off + u); deg = ld_ro(a.row_off + u + 1) - beg; nv++; }
+        if (u < a.n) {
+            beg = ld_ro(a.row_off + u);
+            deg = ld_ro(a.row_off + u + 1) - beg;
+            if (MAXD > 0 && deg > (uint32_t)MAXD) deg = MAXD;
+            nv++;
+        }
         uint32_t incl = deg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -126,11 +132,11 @@ __global__ void k_cc_sample(Args a) {
     flush_counters<256>(a, nv, ne, nu, false, false);
 }
 
-// The label of the largest component, estimated from 4096 hashed samples
+// The label of the largest component, estimated from 1024 hashed samples
 // (mode of their roots).  One CTA of 1024 threads.  Correctness does not
 // depend on the estimate: it only decides which vertices may skip.
 __global__ void k_cc_giant(Args a) {
-    constexpr int S = 4096;
+    constexpr int S = 1024;   // Afforest samples 1024: the mode is the giant whenever one exists
     __shared__ uint32_t s_lab[S];
     __shared__ unsigned long long s_best;
     if (threadIdx.x == 0) s_best = 0;

@@ -588,7 +588,7 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
             relax_mark("cc_edge");
             cc_passes = 1;
         } else {
-            launch_l2(g, k_cc_sample<2>, g->grid_small, s, a);
+            launch_l2(g, k_cc_vertex<BLOCK, 2>, g->grid_cc, s, a);   // sampling: first 2 arcs of every row
             relax_mark("cc_sample");
             launch_l2(g, k_compress, g->grid_small, s, a);
             other_mark("compress");

@@ -1,4 +1,2 @@
-run() { timeout 600 python tools/survey.py --configs $4 --algos $1 --styles $2 --reps 3 2>&1 | grep -v "==" | sed "s/^/$3 /"; }
-for D in 16 32 64 128; do
-FALCON_DENSE_DIV=$D run sssp,bfs worklist dense$D rand-25M,rmat-10M,grid-24M
-done
+timeout 900 python -m pytest tests -m gpu -x -q -k "not full_config" 2>&1 | tail -1
+timeout 600 python tools/survey.py --algos cc --reps 5 2>&1 | grep -v "=="
