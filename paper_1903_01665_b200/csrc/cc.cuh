@@ -112,26 +112,6 @@ __global__ void __launch_bounds__(B) k_cc_edge(Args a) {
     flush_counters<B>(a, 0ull, ne, nu, false, false);
 }
 
-// WORKLIST, sampling (Afforest-style neighbour sampling): every vertex
-// hooks to its first NS out-neighbours
-template <int NS>
-__global__ void k_cc_sample(Args a) {
-    unsigned long long nv = 0, ne = 0, nu = 0;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < a.n; u += stride) {
-        const uint32_t b0 = ld_ro(a.row_off + u), b1 = ld_ro(a.row_off + u + 1);
-        nv++;
-#pragma unroll
-        for (uint32_t r = 0; r < NS; r++) {
-            if (b1 - b0 > r) {
-                ne++;
-                if (uf_unite(a.val, u, ld_ro(a.col + b0 + r))) nu++;
-            }
-        }
-    }
-    flush_counters<256>(a, nv, ne, nu, false, false);
-}
-
 // The label of the largest component, estimated from 1024 hashed samples
 // (mode of their roots).  One CTA of 1024 threads.  Correctness does not
 // depend on the estimate: it only decides which vertices may skip.
