@@ -437,8 +437,27 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     k_scan_local<<<ntiles, 256, 0, s>>>(g->rowb, len, tiles);
     k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
     k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(g->rowb, len, tiles);
-    k_blk_scatter<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->cw, bsz, (uint32_t)K, g->rowb, g->cwb,
-                                                   g->srcb);
+    {   // arcs grouped by target block, CSR order kept inside each block: a
+        // stable radix sort of the arc indices by block id, then a gather
+        uint8_t *keys = nullptr, *keys_out = nullptr;
+        uint32_t *perm_in = nullptr, *perm = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_bytes = 0;
+        int end_bit = 1;
+        while ((1ull << end_bit) < K) end_bit++;
+        CU(dmalloc(&keys, m));
+        CU(dmalloc(&keys_out, m));
+        CU(dmalloc(&perm_in, m));
+        CU(dmalloc(&perm, m));
+        k_blk_keys<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->col, bsz, keys, perm_in);
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_out, perm_in, perm, (int64_t)m, 0, end_bit,
+                                           s));
+        CU(dev_alloc(&tmp, tmp_bytes));
+        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, perm_in, perm, (int64_t)m, 0, end_bit, s));
+        k_blk_gather<<<g->num_sms * 8, BLOCK, 0, s>>>(m, perm, g->cw, g->src, g->cwb, g->srcb);
+        CU(cudaStreamSynchronize(s));
+        dfree(keys); dfree(keys_out); dfree(perm_in); dfree(perm); dfree(tmp);
+    }
     CU(dmalloc(&g->chunkb, (size_t)((m + ECH_SSSP - 1) / ECH_SSSP)));
     k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH_SSSP, g->srcb, g->chunkb);
     CU(cudaGetLastError());
@@ -448,23 +467,17 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     return FALCON_OK;
 }
 
-// Reverse CSR (in-arcs: BFS pull, CC worklist), built once on the device:
-// in-degree histogram + scan for the offsets, and a stable LSD radix sort of
-// the (target, source) arc pairs by target (CUB) for the in-neighbours -- the
-// in-row of v lists its sources in ascending order.
+// Reverse CSR (in-arcs: BFS pull, CC worklist), built once on the device: a
+// stable LSD radix sort of the (target, source) arc pairs by target (CUB) --
+// the in-row of v lists its sources in ascending order -- and the offsets
+// read off the sorted targets.
 falcon_status_t ensure_reverse(falcon_graph *g) {
     if (g->rin_off) return FALCON_OK;
     const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
     cudaStream_t s = g->stream;
     CU(dmalloc(&g->rin_off, n + 1));
     CU(dmalloc(&g->rin_col, m));
-    uint32_t *tiles = g->tiles;
-    const uint32_t ntiles = (uint32_t)((n + 1 + 1023) / 1024);
-    CU(cudaMemsetAsync(g->rin_off, 0, (n + 1) * 4, s));
-    if (m) k_indeg<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->col, g->rin_off);
-    k_scan_local<<<ntiles, 256, 0, s>>>(g->rin_off, n + 1, tiles);
-    k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
-    k_scan_add<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(g->rin_off, n + 1, tiles);
+    if (!m) CU(cudaMemsetAsync(g->rin_off, 0, (n + 1) * 4, s));
     if (m) {
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
@@ -479,6 +492,9 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
         CU(dev_alloc(&tmp, tmp_bytes));
         CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, g->col, keys_out, g->src, g->rin_col, (int64_t)m, 0,
                                            end_bit, s));
+        // in-row offsets from the sorted targets (first position of every
+        // target, vertices without in-arcs included) -- no atomics
+        k_rin_off<<<g->num_sms * 8, BLOCK, 0, s>>>(m, (uint32_t)n, keys_out, g->rin_off);
         CU(cudaStreamSynchronize(s));
         dfree(keys_out);
         dfree(tmp);

@@ -1150,12 +1150,6 @@ __global__ void k_interleave(uint64_t m, const uint32_t *col, const int32_t *w, 
         cw[e] = make_uint2(col[e], (uint32_t)w[e]);
 }
 
-// Reverse CSR (in-arcs), built on the device: in-degree histogram, scan,
-// scatter (in-row order is arbitrary: BFS levels do not depend on it).
-__global__ void k_indeg(uint64_t m, const uint32_t *col, uint32_t *cnt) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) atomicAdd(cnt + col[e], 1u);
-}
 // exclusive scan of x[0..len) in place, tiles of 1024 (two-level, second
 // level over tile sums done by k_scan_tiles with one CTA)
 __global__ void k_scan_local(uint32_t *x, uint64_t len, uint32_t *tile_sums) {
@@ -1208,21 +1202,34 @@ __global__ void k_blk_count(uint32_t n, const uint32_t *row_off, const uint32_t 
     }
     if (blockIdx.x == 0 && threadIdx.x < nblk) cnt[threadIdx.x * ld + n] = 0;
 }
-__global__ void k_blk_scatter(uint32_t n, const uint32_t *row_off, const uint2 *cw, uint32_t bsz, uint32_t nblk,
-                              const uint32_t *rowb, uint2 *cwb, uint32_t *srcb) {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint64_t ld = (uint64_t)n + 1;
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
-        uint32_t pos[MAX_BLK];
-        for (uint32_t k = 0; k < nblk; k++) pos[k] = rowb[k * ld + u];
-        const uint32_t e1 = row_off[u + 1];
-        for (uint32_t e = row_off[u]; e < e1; e++) {
-            const uint2 x = cw[e];
-            const uint32_t k = x.x / bsz;
-            cwb[pos[k]] = x;
-            srcb[pos[k]] = u;
-            pos[k]++;
-        }
+// Blocked layout by sorting (ensure_blocked): block id of every arc's target
+// and the identity permutation, then the gather of the sorted order.
+__global__ void k_blk_keys(uint64_t m, const uint32_t *col, uint32_t bsz, uint8_t *keys, uint32_t *perm) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        keys[e] = (uint8_t)(col[e] / bsz);
+        perm[e] = (uint32_t)e;
+    }
+}
+__global__ void k_blk_gather(uint64_t m, const uint32_t *perm, const uint2 *cw, const uint32_t *src, uint2 *cwb,
+                             uint32_t *srcb) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const uint32_t e = perm[i];
+        cwb[i] = cw[e];
+        srcb[i] = src[e];
+    }
+}
+
+// Offsets of a CSR whose m arcs have the sorted targets key[]: off[v] = first
+// position with key >= v, off[n] = m.  Thread i fills the offsets of the
+// targets in (key[i-1], key[i]].
+__global__ void k_rin_off(uint64_t m, uint32_t n, const uint32_t *key, uint32_t *off) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += stride) {
+        const uint32_t lo = i == 0 ? 0u : key[i - 1] + 1u;
+        const uint32_t hi = i == m ? n : key[i];
+        for (uint32_t v = lo; v <= hi; v++) off[v] = (uint32_t)i;
     }
 }
 

@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "not full_config" 2>&1 | tail -1
-timeout 600 python tools/survey.py --algos cc --reps 5 2>&1 | grep -v "=="
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
+python tools/e2e_timing.py > gpurun_out/e2e_timing.log 2>&1
