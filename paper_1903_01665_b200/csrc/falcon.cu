@@ -39,6 +39,7 @@ constexpr int UNROLL = 4;   // arcs per thread per expansion step
 constexpr int EDGE_QP_SSSP = 1, EDGE_QP_BFS = 2;
 constexpr uint32_t ECH_SSSP = 128u * EDGE_QP_SSSP, ECH_BFS = 128u * EDGE_QP_BFS;   // arcs per warp chunk
 constexpr int HOST_CHECK_EVERY = 4;
+constexpr uint64_t MAX_BLOCKS_USED = 4;   // destination blocks of the SSSP layout (<= MAX_BLK)
 
 thread_local std::string g_last_error;
 
@@ -420,7 +421,9 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
     if (g->blk_bytes == 0) return FALCON_OK;
     uint64_t K = (4 * n + g->blk_bytes - 1) / g->blk_bytes;
-    if (K > MAX_BLK) K = MAX_BLK;
+    // at most 4 blocks: every block pass re-reads the frontier's row offsets
+    // (rand-125M SSSP VERTEX: 8 blocks of 64 MB 54.6 ms, 4 of 128 MB 38.5 ms)
+    if (K > MAX_BLOCKS_USED) K = MAX_BLOCKS_USED;
     while (K > 1 && K * (n + 1) >= (1ull << 32)) K--;
     if (K <= 1) return FALCON_OK;
     const uint32_t bsz = (uint32_t)(((n + K - 1) / K + 31) / 32 * 32);

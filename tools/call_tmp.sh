@@ -1,3 +1,2 @@
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
-python tools/e2e_timing.py > gpurun_out/e2e_timing.log 2>&1
+timeout 900 python tools/survey.py --configs rand-125M,rmat-50M --algos sssp --styles vertex,worklist,edge --reps 3 2>&1 | grep -v "=="
+timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -k "layouts" 2>&1 | tail -1
