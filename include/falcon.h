@@ -219,7 +219,9 @@ FALCON_API falcon_status_t falcon_mst(falcon_graph_t *g, falcon_style_t style, i
 /* Bucket width Δ of FALCON_STYLE_DELTA (SSSP): vertices with tentative
  * distance < T are relaxed from the near queue, the others wait in a far set
  * until the near queue is empty and T advances to the next non-empty bucket.
- * delta == 0 (default) = max(1, average arc weight).
+ * delta == 0 (default) = start at max(1, average arc weight)
+ * and adapt per bucket (double while rounds are latency-bound, halve while
+ * they relax millions of items); delta > 0 is kept fixed.
  * Errors: INVALID_ARG (g NULL or delta < 0). */
 FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
 

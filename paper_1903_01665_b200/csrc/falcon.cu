@@ -214,6 +214,7 @@ struct falcon_graph {
         a.dense_div = dense_div;
         a.blk_div = blk_div;
         a.wl_noq = wl_noq;
+        a.delta_adapt = delta == 0 ? 1u : 0u;   // auto Δ adapts per bucket; an explicit Δ is kept
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;

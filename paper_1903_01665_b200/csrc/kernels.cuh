@@ -58,6 +58,11 @@ struct Ctrl {
     uint32_t thr;         // DELTA: current bucket threshold T (near: dist < T)
     uint32_t delta;       // DELTA: bucket width
     uint32_t minpend;     // DELTA: min tentative distance parked in the far set
+    uint32_t delta0;      // DELTA: initial bucket width (adaptive mode never goes below it)
+    uint32_t delta_adapt; // DELTA: adapt the bucket width per bucket (auto Δ)
+    uint32_t bk_rounds;   // DELTA: near rounds of the current bucket
+    uint32_t pad2_;
+    unsigned long long bk_items;   // DELTA: items relaxed in the current bucket's near rounds
     uint32_t mode;        // DELTA: MODE_NEAR (relax the near queue) / MODE_SCAN (refill from far)
     uint32_t bar_arrive;  // persistent kernel: CTAs arrived at the grid barrier
     uint32_t bar_gen;     // persistent kernel: barrier generation
@@ -93,6 +98,7 @@ struct Args {
     uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
     uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
+    uint32_t delta_adapt;      // DELTA: adapt the bucket width per bucket (auto Δ)
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
@@ -268,6 +274,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
         c->pull = 0; c->found = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
+        c->delta0 = delta; c->delta_adapt = a.delta_adapt; c->bk_rounds = 0; c->bk_items = 0;
         c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
@@ -994,6 +1001,25 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             c->mode = MODE_NEAR;
         } else if (c->out_len == 0) {    // bucket exhausted: move T to the next non-empty bucket
             more = c->minpend != 0xffffffffu;
+            c->bk_items += c->in_len;
+            c->bk_rounds++;
+            if (c->delta_adapt) {
+                // Adaptive Δ (auto mode): a round costs a fixed ~10 µs of launch
+                // and dependent-latency time, worth ~10^5 relaxed items.  A
+                // bucket whose rounds averaged fewer items was latency-bound:
+                // double Δ (fewer, fuller rounds; road grids).  One whose
+                // rounds averaged millions relaxed many vertices more than
+                // once: halve Δ, not below the initial width.  Any sequence
+                // of thresholds reaches the same fixpoint (T always moves past
+                // the smallest parked distance).
+                const unsigned long long avg = c->bk_items / (c->bk_rounds ? c->bk_rounds : 1u);
+                // (growth capped at 128 x the initial width: on a road grid the
+                // rounds stay small whatever Δ, and a larger Δ only adds work)
+                if (avg < (128ull << 10) && c->delta < 128u * c->delta0 && c->delta < (1u << 26)) c->delta *= 2u;
+                else if (avg > (2ull << 20) && c->delta / 2u >= c->delta0) c->delta /= 2u;
+            }
+            c->bk_items = 0;
+            c->bk_rounds = 0;
             if (more) {
                 const uint64_t t = ((uint64_t)c->minpend / c->delta + 1) * c->delta;
                 c->thr = t > 0x7fffffffull ? 0x7fffffffu : (uint32_t)t;
@@ -1002,6 +1028,8 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             }
         } else {
             more = true;
+            c->bk_items += c->in_len;   // a near round of the current bucket
+            c->bk_rounds++;
         }
     }
     if (c->status != ST_OK) more = false;
