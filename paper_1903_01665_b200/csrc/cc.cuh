@@ -104,10 +104,16 @@ __global__ void __launch_bounds__(B) k_cc_edge(Args a) {
     const uint64_t pf = pol_evict_first();
     unsigned long long ne = 0, nu = 0;
     const uint32_t stride = gridDim.x * B;
-    for (uint32_t e = blockIdx.x * B + threadIdx.x; e < a.m; e += stride) {
-        const uint32_t u = ld_stream(a.src + e, pf), v = ld_stream(a.col + e, pf);
+    uint32_t e = blockIdx.x * B + threadIdx.x;
+    // the next arc's endpoints are loaded while this arc's find chains run
+    uint32_t u = e < a.m ? ld_stream(a.src + e, pf) : 0u, v = e < a.m ? ld_stream(a.col + e, pf) : 0u;
+    for (; e < a.m; e += stride) {
+        const uint32_t en = e + stride;
+        const uint32_t un = en < a.m ? ld_stream(a.src + en, pf) : 0u, vn = en < a.m ? ld_stream(a.col + en, pf) : 0u;
         ne++;
         if (uf_unite(a.val, u, v)) nu++;
+        u = un;
+        v = vn;
     }
     flush_counters<B>(a, 0ull, ne, nu, false, false);
 }
