@@ -665,11 +665,19 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
             auto word_at = [&](uint32_t wi) -> uint32_t {
                 return wi < a.nwords ? (COHERENT ? __ldcg(x.bm_prev + wi) : x.bm_prev[wi]) : 0u;
             };
-            uint32_t wnext = word_at(gw * 32 + lane);   // next group's word, one group ahead
+            // the bitmap words of the next DP groups are in flight (a light
+            // round's groups are mostly empty: one load latency per DP groups)
+            constexpr int DP = 4;
+            uint32_t wq[DP];
+#pragma unroll
+            for (int k = 0; k < DP; k++) wq[k] = word_at(gw * 32 + k * wstride + lane);
             for (uint32_t g0 = gw * 32; g0 < a.nwords; g0 += wstride) {   // warp-uniform
                 const uint32_t wi = g0 + lane;
-                const uint32_t word = wnext;
-                wnext = word_at(g0 + wstride + lane);
+                const uint32_t word = wq[0];
+#pragma unroll
+                for (int k = 0; k < DP - 1; k++) wq[k] = wq[k + 1];
+                wq[DP - 1] = word_at(g0 + DP * wstride + lane);
+                if (!__any_sync(FULL, word != 0u)) continue;
                 const uint32_t cnt = __popc(word);
                 uint32_t incl = cnt;
 #pragma unroll
