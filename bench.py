@@ -58,6 +58,9 @@ def parse():
                          "GPUs with NCCL exchange (SURVEY.md §8(e), strong scaling)")
     ap.add_argument("--simulate", type=int, default=0,
                     help="partition mode on ONE GPU with this many simulated parts (device-side exchange)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for barriers / max-over-ranks (gloo: functional tests of N>1 "
+                         "with several ranks sharing one GPU)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -250,11 +253,15 @@ def main():
     import paper_1903_01665_b200 as fb
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    local = local % torch.cuda.device_count()   # one rank per GPU; ranks may share a GPU in functional tests
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     fb.load()
     algos = [a for a in args.algos.split(",") if a]
     styles = [s for s in args.styles.split(",") if s]
@@ -323,7 +330,7 @@ def main():
             dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
     if dist:
-        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms_total], device="cuda" if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -408,7 +415,7 @@ def main():
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            t = torch.tensor([ems], device="cuda" if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": replicas * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",

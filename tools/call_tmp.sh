@@ -1,2 +1,5 @@
-timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -k "not full_config and not three" 2>&1 | tail -1
-timeout 900 python tools/survey.py --configs rand-25M,rmat-10M,grid-24M --algos sssp,bfs --styles vertex,worklist,delta --reps 3 2>&1 | grep -v "=="
+python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
+for M in replica sections; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 1 --mode $M --dist-backend gloo --no-e2e > gpurun_out/multi_$M.log 2>&1; echo "rc=$?" >> gpurun_out/multi_$M.log
+done
+timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/ref.log 2>&1; echo "rc=$?" >> gpurun_out/ref.log
