@@ -179,6 +179,11 @@ typedef struct {
 FALCON_API falcon_status_t falcon_run_many(int njobs, falcon_graph_t *const *graphs, const falcon_job_t *jobs,
                                            int32_t *const *outs, falcon_stats_t *stats);
 
+/* Return the device memory the library keeps cached for reuse (blocks of
+ * freed graphs and per-call staging) to the CUDA driver; *released_bytes
+ * (nullable) receives the amount.  Live graphs are not affected. */
+FALCON_API falcon_status_t falcon_trim_memory(int64_t *released_bytes);
+
 /* Query vertex / arc counts of a loaded graph. */
 FALCON_API falcon_status_t graph_info(const falcon_graph_t *g, int64_t *n, int64_t *m);
 

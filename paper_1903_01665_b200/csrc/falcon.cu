@@ -1050,6 +1050,20 @@ falcon_status_t graph_free(falcon_graph_t *g) {
     return FALCON_OK;
 }
 
+falcon_status_t falcon_trim_memory(int64_t *released_bytes) {
+    DevCache &c = dev_cache();
+    std::vector<void *> rel;
+    int64_t bytes = 0;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto &kv : c.idle) { rel.push_back(kv.second); bytes += (int64_t)kv.first.second; }
+        c.idle.clear();
+    }
+    for (void *q : rel) cudaFree(q);
+    if (released_bytes) *released_bytes = bytes;
+    return FALCON_OK;
+}
+
 falcon_status_t graph_share(falcon_graph_t *g, const falcon_load_opts_t *opts, falcon_graph_t **out) {
     if (!g || !out) return fail(FALCON_ERR_INVALID_ARG, "graph or out is NULL");
     *out = nullptr;

@@ -153,6 +153,25 @@ def test_parity_worklist_noq(gpu_lib, name, dense_div, wl_noq, persist):
         assert np.array_equal(out, exp), f"{name}/{algo}/dd={dense_div}/noq={wl_noq}: {np.flatnonzero(out != exp)[:10]}"
 
 
+def test_memory_cache_reuse_and_trim(gpu_lib):
+    """graph_free returns device memory to the library's cache; a second graph
+    of the same shape reuses it; falcon_trim_memory hands it back."""
+    import torch
+    G = _graph("rand-s")
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    out, _ = _run(gpu_lib, g, "sssp", "edge", G.source)
+    gpu_lib.graph_free(g)
+    free0 = torch.cuda.mem_get_info()[0]
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)          # served from the cache
+    out2, _ = _run(gpu_lib, g, "sssp", "edge", G.source)
+    assert np.array_equal(out, out2)
+    assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)
+    gpu_lib.graph_free(g)
+    released = gpu_lib.falcon_trim_memory()
+    assert released > 0
+    assert gpu_lib.falcon_trim_memory() == 0
+
+
 def test_set_option_rejects_unknown(gpu_lib):
     G = _graph("tiny")
     g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
