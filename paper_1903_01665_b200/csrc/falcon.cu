@@ -314,9 +314,7 @@ struct Round {
                 launch_coop(g, k_persist<SSSP, DELTA, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div, g->persist_max);
                 launches++;
             }
-            launch_l2(g, k_scan_far<BLOCK>, g->grid_pull, s, a);
-            launches++;
-            if (tr) tr->mark(s, "scan_far", 0);
+            // the far-set refill (MODE_SCAN rounds) runs inside the expansion kernel
             launch_expand_warp<ALGO, DELTA>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == WORKLIST) {

@@ -334,15 +334,6 @@ __device__ __forceinline__ void scan_far_round(const Args &a, Ctrl *c, uint32_t 
     if (lane == 0 && pend_min != 0xffffffffu) atomicMin(&c->minpend, pend_min);
 }
 
-template <int B>
-__global__ void __launch_bounds__(B) k_scan_far(Args a) {
-    Ctrl *c = a.ctrl;
-    if (c->done || c->mode != MODE_SCAN) return;
-    unsigned long long nv = 0;
-    scan_far_round<false>(a, c, c->iter, c->thr, c->sel ? a.fr0 : a.fr1, nv);
-    flush_counters<B>(a, nv, 0ull, 0ull, false, false);
-}
-
 // Sum of the arc weights (auto Δ = max(1, average weight)).
 __global__ void k_sum_weights(uint64_t m, const int32_t *w, unsigned long long *sum) {
     unsigned long long t = 0;
@@ -757,7 +748,13 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     static_assert(STYLE == VERTEX || STYLE == WORKLIST || STYLE == DELTA, "expand is for VERTEX/WORKLIST/DELTA");
     constexpr int WQ = (STYLE == WORKLIST || STYLE == DELTA) ? 256 : 1;
     Ctrl *c = a.ctrl;
-    if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull) || (STYLE == DELTA && c->mode != MODE_NEAR)) return;
+    if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull)) return;
+    if (STYLE == DELTA && c->mode != MODE_NEAR) {   // this round refills the near queue from the far set
+        unsigned long long nv = 0;
+        scan_far_round<false>(a, c, c->iter, c->thr, c->sel ? a.fr0 : a.fr1, nv);
+        flush_counters<B>(a, nv, 0ull, 0ull, false, false);
+        return;
+    }
     const uint32_t iter = c->iter;
     if (STYLE == VERTEX) clear_next_bitmap(a, iter);
     const uint32_t thr = STYLE == DELTA ? c->thr : 0xffffffffu;
