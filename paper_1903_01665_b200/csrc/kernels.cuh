@@ -285,7 +285,8 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
 // as a near/far worklist: the near queue holds vertices below the bucket
 // threshold T, improved vertices at or beyond T are parked in the far set
 // (a bitmap).  When the near queue runs dry, k_advance moves T to the bucket
-// of the smallest parked distance and this kernel moves every parked vertex
+// of the smallest parked distance and this pass (run by k_expand_warp in a
+// scan round) moves every parked vertex
 // now below T into the near queue (one warp per 32-vertex word: the far word
 // is rewritten with a plain store), recomputing the minimum of what stays.
 template <bool COHERENT>
