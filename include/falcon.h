@@ -143,6 +143,12 @@ FALCON_API falcon_status_t falcon_comm_free(falcon_comm_t *comm);
  * simulated graph). */
 FALCON_API falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi);
 
+/* Bytes the last call on a partitioned graph moved in its boundary exchanges
+ * (dense reduce-scatter rounds: 4 bytes per exchanged vertex; sparse rounds:
+ * 8 bytes per (vertex, value) pair; this rank's sends, or all parts when
+ * simulated).  0 for a single-GPU graph. */
+FALCON_API falcon_status_t graph_exchange_bytes(const falcon_graph_t *g, int64_t *bytes);
+
 /* Release the graph's device memory (to the library's device-memory cache,
  * which later loads reuse; a failed allocation releases the cache).  NULL is a
  * no-op.  Errors: INVALID_ARG if views created by graph_share are still live. */
@@ -246,6 +252,9 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *   "persist_max"  ... while the frontier holds at most this many items
  * Changing an option drops the cached CUDA graphs (and, for block_bytes, the
  * blocked layout); they are rebuilt on the next call.
+ *   "exchange"     partitioned graphs: boundary exchange per superstep, 0 = auto
+ *                  (sparse pairs when smaller than the dense reduce-scatter),
+ *                  1 = dense, 2 = sparse (env FALCON_EXCHANGE)
  *   "wl_noq"       WORKLIST dense rounds mark the next bitmap without claims
  *                  or a queue (default 1, env FALCON_WL_NOQ; 0 = off)
  * Errors: INVALID_ARG (g/name NULL, value out of range), UNSUPPORTED (unknown

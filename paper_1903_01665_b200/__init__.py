@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "graph_share", "falcon_run_many", "falcon_mst", "falcon_trim_memory", "falcon_sssp", "falcon_bfs", "falcon_cc",
+__all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "graph_share", "falcon_run_many", "falcon_mst", "falcon_trim_memory", "graph_exchange_bytes", "falcon_sssp", "falcon_bfs", "falcon_cc",
            "falcon_set_profiling", "falcon_set_delta", "falcon_set_option", "falcon_partition", "falcon_comm_unique_id",
            "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_free", "graph_owned_range", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
@@ -89,6 +89,8 @@ def load(build_if_missing: bool = False):
     lib.falcon_comm_init_simulated.argtypes = [ctypes.c_int, ctypes.POINTER(p)]
     lib.falcon_comm_free.argtypes = [p]
     lib.graph_owned_range.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.graph_exchange_bytes.argtypes = [p, ctypes.POINTER(i64)]
+    lib.graph_exchange_bytes.restype = st
     lib.falcon_trim_memory.argtypes = [ctypes.POINTER(i64)]
     lib.falcon_trim_memory.restype = st
     lib.falcon_mst.argtypes = [p, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64), p,
@@ -301,6 +303,13 @@ def falcon_cc(g: Graph, style, label_out) -> FalconStats:
     _check_dtype(label_out, "i32", "label_out")
     _check(load().falcon_cc(g.handle, _style(style), _ptr(label_out), ctypes.byref(st)))
     return st
+
+
+def graph_exchange_bytes(g: Graph) -> int:
+    """Bytes the last call on a partitioned graph moved in boundary exchanges."""
+    out = ctypes.c_int64()
+    _check(load().graph_exchange_bytes(g.handle, ctypes.byref(out)))
+    return out.value
 
 
 def falcon_trim_memory() -> int:

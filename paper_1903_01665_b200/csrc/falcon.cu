@@ -198,6 +198,17 @@ struct falcon_graph {
     int32_t *recv = nullptr;              // (part) owned-range receive buffer of the exchange
     uint2 *cw_unit = nullptr;             // (part) unit-weight (col, 1) arcs: BFS as unit-weight SSSP
     bool use_unit = false;
+    // sparse exchange (partition.cuh): (part) per-owner counts, outbox of (vertex,
+    // value) pairs in per-owner regions, NCCL inbox; (partitioned handle)
+    // device copies of the bounds and, simulated, tables of every part's buffers
+    uint32_t *xcounts = nullptr, *xcnt_recv = nullptr;
+    uint2 *outbox = nullptr, *inbox = nullptr;
+    uint32_t *bounds_d = nullptr;
+    unsigned long long *xpairs_d = nullptr;   // (simulated) pairs packed by sparse rounds of the current call
+    uint2 **d_outboxes = nullptr;
+    uint32_t **d_counts = nullptr;
+    uint32_t exchange = 0;                // 0 auto, 1 dense, 2 sparse (FALCON_EXCHANGE / option "exchange")
+    uint64_t xbytes = 0;                  // bytes moved by the exchanges of the last call (all ranks' share here)
 
     Args args() const {
         Args a{};
@@ -827,7 +838,9 @@ void destroy(falcon_graph *g) {
                     (void *)g->rin_off, (void *)g->rin_col, (void *)g->rowb, (void *)g->cwb, (void *)g->srcb,
                     (void *)g->chunk, (void *)g->chunkb, (void *)g->chunks, (void *)g->val, (void *)g->bm,
                     (void *)g->fr0, (void *)g->fr1, (void *)g->tiles, (void *)g->ctrl, (void *)g->cnt,
-                    (void *)g->d_flags, (void *)g->mst_best, (void *)g->mst_list})
+                    (void *)g->d_flags, (void *)g->mst_best, (void *)g->mst_list, (void *)g->xcounts,
+                    (void *)g->xcnt_recv, (void *)g->outbox, (void *)g->inbox, (void *)g->bounds_d,
+                    (void *)g->d_outboxes, (void *)g->d_counts})
         dfree(p);   // back to the device cache (the stream was synchronised above)
     if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -1110,6 +1123,12 @@ falcon_status_t falcon_run_many(int njobs, falcon_graph_t *const *graphs, const 
     return FALCON_OK;
 }
 
+falcon_status_t graph_exchange_bytes(const falcon_graph_t *g, int64_t *bytes) {
+    if (!g || !bytes) return fail(FALCON_ERR_INVALID_ARG, "graph or bytes is NULL");
+    *bytes = g->comm ? (int64_t)g->xbytes : 0;
+    return FALCON_OK;
+}
+
 falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi) {
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (lo) *lo = g->comm ? g->lo : 0;
@@ -1220,6 +1239,9 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->dense_div = (uint32_t)value;
         } else if (!strcmp(name, "block_div")) {
             t->blk_div = (uint32_t)value;
+        } else if (!strcmp(name, "exchange")) {
+            if (value > 2) return fail(FALCON_ERR_INVALID_ARG, "exchange: 0 auto, 1 dense, 2 sparse");
+            g->exchange = (uint32_t)value;
         } else if (!strcmp(name, "wl_noq")) {
             t->wl_noq = (uint32_t)(value != 0);
         } else if (!strcmp(name, "pull_div")) {

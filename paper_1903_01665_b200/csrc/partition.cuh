@@ -51,6 +51,8 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -67,7 +69,7 @@ NcclApi *nccl_api() {
     if (!api.h) return nullptr;
 #define SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))
     SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(Reduce); SYM(AllReduce);
-    SYM(Broadcast); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString);
+    SYM(Broadcast); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString); SYM(Send); SYM(Recv);
 #undef SYM
     if (!api.GetUniqueId || !api.CommInitRank || !api.Reduce || !api.AllReduce || !api.Broadcast ||
         !api.GroupStart || !api.GroupEnd) {
@@ -133,6 +135,109 @@ __global__ void k_sim_sum_changed(Ctrl *const *ctrls, int nparts) {
     for (int p = 0; p < nparts; p++) ctrls[p]->changed = s;
 }
 
+// ------------------------------------------------------------------ sparse exchange
+// The remote vertices a part improved in this round are exactly the bits of
+// bm[iter % 3] outside its owned range [lo, hi).  When their (vertex, value)
+// pairs -- 8 bytes each -- are fewer bytes than the dense reduce-scatter
+// (4 n (P-1) / P per rank), only they travel; MIN is idempotent, so a round
+// may use either exchange.
+
+__device__ __forceinline__ int owner_of(const uint32_t *bounds, int P, uint32_t v) {
+    int lo = 0, hi = P;   // largest q with bounds[q] <= v
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (bounds[mid] <= v) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// counts[q] = remote improved vertices owned by q (PACK: also write the pairs
+// into outbox[bounds[q] + slot]); one word per thread, aggregated per word
+template <bool PACK>
+__global__ void k_remote_pairs(Args a, uint32_t lo, uint32_t hi, const uint32_t *bounds, int P, uint32_t *counts,
+                               uint2 *outbox) {
+    Ctrl *c = a.ctrl;
+    if (c->done) return;
+    const uint32_t *bm_now = bm_of(a, c->iter);
+    const uint32_t nw = (a.n + 31) / 32, stride = gridDim.x * blockDim.x;
+    for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += stride) {
+        uint32_t word = bm_now[wi];
+        if (!word) continue;
+        const uint32_t vb = wi * 32;
+        // drop the owned bits and the bits past n
+        for (uint32_t b = 0; b < 32; b++) {
+            const uint32_t v = vb + b;
+            if (v >= a.n || (v >= lo && v < hi)) word &= ~(1u << b);
+        }
+        while (word) {   // runs of bits with one owner
+            const uint32_t v0 = vb + (uint32_t)(__ffs(word) - 1);
+            const int q = owner_of(bounds, P, v0);
+            const uint32_t qend = bounds[q + 1];
+            uint32_t sub = word;
+            if (qend < vb + 32) sub &= (qend > vb ? ((1u << (qend - vb)) - 1u) : 0u);
+            word &= ~sub;
+            const uint32_t k = (uint32_t)__popc(sub);
+            const uint32_t slot = atomicAdd(counts + q, k);
+            if (PACK) {
+                uint32_t i = 0;
+                for (uint32_t y = sub; y; y &= y - 1, i++) {
+                    const uint32_t v = vb + (uint32_t)(__ffs(y) - 1);
+                    outbox[bounds[q] + slot + i] = make_uint2(v, (uint32_t)a.val[v]);
+                }
+            }
+        }
+    }
+}
+
+// statistics (simulated): pairs packed this round, summed over every part
+__global__ void k_sum_counts(const uint32_t *const *counts, int P, unsigned long long *total) {
+    unsigned long long t = 0;
+    for (int i = threadIdx.x; i < P * P; i += blockDim.x) t += counts[i / P][i % P];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(total, t);
+}
+
+// owner side: apply received pairs (atomicMin, mark improved)
+__global__ void k_apply_pairs(Args a, const uint2 *pairs, uint32_t cnt) {
+    Ctrl *c = a.ctrl;
+    if (c->done) return;
+    uint32_t *bm_now = bm_of(a, c->iter);
+    bool chg = false;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+        const uint2 p = pairs[i];
+        if ((int32_t)p.y < a.val[p.x] && (int32_t)p.y < atomicMin(a.val + p.x, (int32_t)p.y)) {
+            atomicOr(bm_now + (p.x >> 5), 1u << (p.x & 31));
+            chg = true;
+        }
+    }
+    if (__syncthreads_or(chg) && threadIdx.x == 0) c->changed = 1;
+}
+
+// simulated: owner q applies every part's pairs for q straight from their outboxes
+__global__ void k_sim_apply_pairs(Args a, const uint2 *const *outboxes, const uint32_t *const *counts, int P, int q,
+                                  uint32_t qlo) {
+    Ctrl *c = a.ctrl;
+    if (c->done) return;
+    uint32_t *bm_now = bm_of(a, c->iter);
+    bool chg = false;
+    for (int p = 0; p < P; p++) {
+        if (p == q) continue;
+        const uint32_t cnt = counts[p][q];
+        const uint2 *pairs = outboxes[p] + qlo;
+        const uint32_t stride = gridDim.x * blockDim.x;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+            const uint2 x = pairs[i];
+            if ((int32_t)x.y < a.val[x.x] && (int32_t)x.y < atomicMin(a.val + x.x, (int32_t)x.y)) {
+                atomicOr(bm_now + (x.x >> 5), 1u << (x.x & 31));
+                chg = true;
+            }
+        }
+    }
+    if (__syncthreads_or(chg) && threadIdx.x == 0) c->changed = 1;
+}
+
 // ------------------------------------------------------------------ host side
 // Boundaries of nparts contiguous vertex ranges with ~m/nparts arcs each:
 // boundary q is the vertex v >= bounds[q-1] whose prefix row_off[v] is
@@ -166,6 +271,41 @@ void destroy_partitioned(falcon_graph *g) {
         destroy(p);
     }
     g->parts.clear();
+    dfree(g->bounds_d); dfree(g->d_outboxes); dfree(g->d_counts); dfree(g->xpairs_d);
+    g->bounds_d = nullptr; g->d_outboxes = nullptr; g->d_counts = nullptr; g->xpairs_d = nullptr;
+}
+
+// Buffers of the sparse exchange, allocated on first use.
+falcon_status_t ensure_sparse(falcon_graph *g) {
+    if (g->bounds_d) return FALCON_OK;
+    falcon_comm *cm = g->comm;
+    const int P = cm->simulated ? cm->simulated : cm->nranks;
+    cudaStream_t s = g->parts[0]->stream;
+    std::vector<uint32_t> hb((size_t)P + 1);
+    for (int q = 0; q <= P; q++) hb[(size_t)q] = (uint32_t)g->bounds[(size_t)q];
+    CU(dmalloc(&g->bounds_d, (size_t)P + 1));
+    CU(dmalloc(&g->xpairs_d, 1));
+    CU(cudaMemcpyAsync(g->bounds_d, hb.data(), (size_t)(P + 1) * 4, cudaMemcpyHostToDevice, s));
+    std::vector<uint2 *> ho;
+    std::vector<uint32_t *> hc;
+    for (auto *p : g->parts) {
+        CU(dmalloc(&p->xcounts, (size_t)P));
+        CU(dmalloc(&p->outbox, (size_t)g->n));
+        if (!cm->simulated) {
+            CU(dmalloc(&p->xcnt_recv, (size_t)P));
+            CU(dmalloc(&p->inbox, (size_t)(p->hi - p->lo) * (size_t)(P > 1 ? P - 1 : 1) + 1));
+        }
+        ho.push_back(p->outbox);
+        hc.push_back(p->xcounts);
+    }
+    if (cm->simulated) {
+        CU(dmalloc(&g->d_outboxes, (size_t)P));
+        CU(dmalloc(&g->d_counts, (size_t)P));
+        CU(cudaMemcpyAsync(g->d_outboxes, ho.data(), sizeof(uint2 *) * P, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(g->d_counts, hc.data(), sizeof(uint32_t *) * P, cudaMemcpyHostToDevice, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    return FALCON_OK;
 }
 
 // Build the part owning [lo, hi): its rows only, global ids, full n.
@@ -230,6 +370,103 @@ falcon_status_t load_partitioned(int64_t n, int64_t m, const uint32_t *row_off, 
     g->lo = cm->simulated ? 0 : g->bounds[cm->rank];
     g->hi = cm->simulated ? n : g->bounds[cm->rank + 1];
     g->stream = g->parts[0]->stream;
+    if (const char *ex = getenv("FALCON_EXCHANGE")) g->exchange = (uint32_t)atoi(ex) % 3u;
+    return FALCON_OK;
+}
+
+// Per-owner counts of the remote vertices each part improved this round, and
+// the decision: sparse when their pairs (8 B each) are fewer bytes than the
+// dense exchange (4 n (P-1) bytes over all ranks), or when forced.
+falcon_status_t exchange_counts(falcon_graph *g, const std::vector<Args> &args, cudaStream_t s, bool *sparse) {
+    falcon_comm *cm = g->comm;
+    const int P = cm->simulated ? cm->simulated : cm->nranks;
+    falcon_status_t st = ensure_sparse(g);
+    if (st != FALCON_OK) return st;
+    if (g->exchange == 2) { *sparse = true; return FALCON_OK; }
+    // simulated parts share one device's memory: the dense device-side reduce
+    // costs no interconnect traffic, a per-round decision would only add host
+    // synchronisation -- auto is dense there (sparse stays selectable)
+    if (cm->simulated) { *sparse = false; return FALCON_OK; }
+    unsigned long long total = 0;
+    std::vector<uint32_t> h((size_t)P);
+    for (size_t i = 0; i < g->parts.size(); i++) {
+        falcon_graph *p = g->parts[i];
+        CU(cudaMemsetAsync(p->xcounts, 0, (size_t)P * 4, s));
+        k_remote_pairs<false><<<p->grid_small, BLOCK, 0, s>>>(args[i], (uint32_t)p->lo, (uint32_t)p->hi, g->bounds_d,
+                                                              P, p->xcounts, nullptr);
+    }
+    if (cm->simulated) {
+        for (auto *p : g->parts) {
+            CU(cudaMemcpyAsync(h.data(), p->xcounts, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            for (int q = 0; q < P; q++) total += h[(size_t)q];
+        }
+    } else {   // the decision must be the same on every rank: all-reduce the local totals
+        NcclApi *nc = nccl_api();
+        falcon_graph *me = g->parts[0];
+        CU(cudaMemcpyAsync(h.data(), me->xcounts, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        unsigned long long local = 0;
+        for (int q = 0; q < P; q++) local += h[(size_t)q];
+        unsigned long long *d_tot = reinterpret_cast<unsigned long long *>(me->xcnt_recv);   // P >= 2 words
+        CU(cudaMemcpyAsync(d_tot, &local, 8, cudaMemcpyHostToDevice, s));
+        NC(nc->AllReduce(d_tot, d_tot, 1, ncclUint64, ncclSum, cm->nccl, s));
+        CU(cudaMemcpyAsync(&total, d_tot, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    *sparse = 8ull * total < 4ull * (uint64_t)g->n * (uint64_t)(P - 1);
+    return FALCON_OK;
+}
+
+// Sparse exchange: pack the pairs per owner, move them (device reads when
+// simulated; grouped ncclSend / ncclRecv after a count exchange otherwise),
+// apply them on the owners with atomicMin.
+falcon_status_t exchange_sparse(falcon_graph *g, const std::vector<Args> &args, cudaStream_t s) {
+    falcon_comm *cm = g->comm;
+    const int P = cm->simulated ? cm->simulated : cm->nranks;
+    for (size_t i = 0; i < g->parts.size(); i++) {
+        falcon_graph *p = g->parts[i];
+        CU(cudaMemsetAsync(p->xcounts, 0, (size_t)P * 4, s));
+        k_remote_pairs<true><<<p->grid_small, BLOCK, 0, s>>>(args[i], (uint32_t)p->lo, (uint32_t)p->hi, g->bounds_d, P,
+                                                             p->xcounts, p->outbox);
+    }
+    if (cm->simulated) {
+        for (int q = 0; q < P; q++) {
+            falcon_graph *p = g->parts[(size_t)q];
+            k_sim_apply_pairs<<<p->grid_small, BLOCK, 0, s>>>(args[(size_t)q], g->d_outboxes, g->d_counts, P, q,
+                                                              (uint32_t)p->lo);
+        }
+        k_sum_counts<<<1, 64, 0, s>>>(g->d_counts, P, g->xpairs_d);   // bytes moved, read once per call
+        return FALCON_OK;
+    }
+    NcclApi *nc = nccl_api();
+    if (!nc->Send || !nc->Recv) return fail(FALCON_ERR_COMM, "ncclSend/ncclRecv unavailable");
+    falcon_graph *me = g->parts[0];
+    const int r = cm->rank;
+    NC(nc->GroupStart());   // counts: what every peer sends to me
+    for (int q = 0; q < P; q++) {
+        if (q == r) continue;
+        NC(nc->Send(me->xcounts + q, 1, ncclUint32, q, cm->nccl, s));
+        NC(nc->Recv(me->xcnt_recv + q, 1, ncclUint32, q, cm->nccl, s));
+    }
+    NC(nc->GroupEnd());
+    std::vector<uint32_t> hs((size_t)P), hr((size_t)P);
+    CU(cudaMemcpyAsync(hs.data(), me->xcounts, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hr.data(), me->xcnt_recv, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    uint64_t in_total = 0;
+    NC(nc->GroupStart());   // payloads: my pairs for q from my outbox region q, q's pairs for me into my inbox
+    for (int q = 0; q < P; q++) {
+        if (q == r) continue;
+        if (hs[(size_t)q])
+            NC(nc->Send(me->outbox + g->bounds[(size_t)q], 2 * (size_t)hs[(size_t)q], ncclUint32, q, cm->nccl, s));
+        if (hr[(size_t)q])
+            NC(nc->Recv(me->inbox + in_total, 2 * (size_t)hr[(size_t)q], ncclUint32, q, cm->nccl, s));
+        in_total += hr[(size_t)q];
+        g->xbytes += 8ull * hs[(size_t)q];
+    }
+    NC(nc->GroupEnd());
+    if (in_total) k_apply_pairs<<<me->grid_small, BLOCK, 0, s>>>(args[0], me->inbox, (uint32_t)in_total);
     return FALCON_OK;
 }
 
@@ -262,6 +499,8 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         CU(cudaMemcpyAsync(d_ctrls, hc.data(), sizeof(Ctrl *) * P, cudaMemcpyHostToDevice, s));
     }
     CU(cudaEventRecord(g->parts[0]->ev0, s));
+    g->xbytes = 0;
+    if (g->xpairs_d) CU(cudaMemsetAsync(g->xpairs_d, 0, 8, s));
     const int init_algo = algo == CC ? CC : SSSP;
     for (size_t i = 0; i < g->parts.size(); i++) {
         falcon_graph *p = g->parts[i];
@@ -292,13 +531,25 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
                 for (size_t i = 0; i < g->parts.size(); i++)
                     launch_l2(g->parts[i], k_compress, g->parts[i]->grid_small, s, args[i]);
             } else {
-                if (cm->simulated) {
+                // dense reduce-scatter or sparse (vertex, value) pairs, decided per round
+                bool sparse = false;
+                const int NP = cm->simulated ? P : cm->nranks;
+                if (g->exchange != 1 && NP > 1) {
+                    falcon_status_t st = exchange_counts(g, args, s, &sparse);
+                    if (st != FALCON_OK) return st;
+                }
+                if (sparse) {
+                    falcon_status_t st = exchange_sparse(g, args, s);
+                    if (st != FALCON_OK) return st;
+                } else if (cm->simulated) {
+                    g->xbytes += 4ull * (uint64_t)g->n * (uint64_t)(P - 1);
                     for (int q = 0; q < P; q++) {
                         falcon_graph *p = g->parts[(size_t)q];
                         k_sim_reduce_min<<<p->grid_small, BLOCK, 0, s>>>(d_vals, P, (uint32_t)p->lo,
                                                                            (uint32_t)(p->hi - p->lo), p->recv);
                     }
                 } else {
+                    g->xbytes += 4ull * (uint64_t)(g->n - (g->hi - g->lo));
                     falcon_graph *me = g->parts[0];
                     NC(nc->GroupStart());
                     for (int q = 0; q < cm->nranks; q++) {
@@ -308,7 +559,7 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
                     }
                     NC(nc->GroupEnd());
                 }
-                for (size_t i = 0; i < g->parts.size(); i++) {
+                for (size_t i = 0; i < g->parts.size() && !sparse; i++) {
                     falcon_graph *p = g->parts[i];
                     if (p->hi > p->lo)
                         k_apply_owned<<<p->grid_small, BLOCK, 0, s>>>(args[i], p->recv, (uint32_t)p->lo,
@@ -336,6 +587,12 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
     }
     for (size_t i = 0; i < g->parts.size(); i++)
         k_finish<<<1, BLOCK, 0, s>>>(args[i], (uint32_t)g->parts[i]->cnt_slots);
+    if (cm->simulated && g->xpairs_d) {
+        unsigned long long pairs = 0;
+        CU(cudaMemcpyAsync(&pairs, g->xpairs_d, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        g->xbytes += 8ull * pairs;
+    }
     // gather: the full array on every rank
     int32_t *dst = out;
     int32_t *staging = nullptr;
