@@ -74,7 +74,9 @@ typedef struct falcon_graph falcon_graph_t; /* opaque; owns its device memory */
 typedef struct falcon_comm falcon_comm_t;   /* opaque; multi-GPU communicator (NULL = single GPU) */
 
 /* graph_load_csr options (pass NULL for defaults). */
-#define FALCON_LOAD_BUILD_COO 0x1u  /* build the COO src[] array now (else lazily on first EDGE call) */
+#define FALCON_LOAD_BUILD_COO 0x1u      /* build the COO src[] array now (else lazily on first EDGE call) */
+#define FALCON_LOAD_BUILD_REVERSE 0x2u  /* build the reverse (in-arc) CSR now (else lazily on the first BFS
+                                           VERTEX / CC WORKLIST call) */
 
 typedef struct {
     int device;          /* CUDA device ordinal; -1 = current device                 */

@@ -24,6 +24,7 @@ INF = 2147483647
 STYLE_VERTEX, STYLE_EDGE, STYLE_WORKLIST, STYLE_DELTA = 0, 1, 2, 3
 STYLES = {"vertex": STYLE_VERTEX, "edge": STYLE_EDGE, "worklist": STYLE_WORKLIST, "delta": STYLE_DELTA}
 LOAD_BUILD_COO = 0x1
+LOAD_BUILD_REVERSE = 0x2
 ALGOS = {"sssp": 0, "bfs": 1, "cc": 2}
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "NO_MEMORY", 4: "CUDA", 5: "OVERFLOW",
           6: "NOT_CONVERGED", 7: "COMM", 8: "UNSUPPORTED"}

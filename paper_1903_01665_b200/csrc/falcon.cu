@@ -966,6 +966,10 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (flags & 1) return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must start at 0, be nondecreasing and end at m");
     if (flags & 2) return fail(FALCON_ERR_OUT_OF_RANGE, "col[e] >= n");
     if (flags & 4) return fail(FALCON_ERR_OUT_OF_RANGE, "negative weight");
+    if (opts && (opts->flags & FALCON_LOAD_BUILD_REVERSE)) {
+        falcon_status_t st = ensure_reverse(g);
+        if (st != FALCON_OK) return st;
+    }
     if (opts && (opts->flags & FALCON_LOAD_BUILD_COO)) {
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
@@ -1038,7 +1042,7 @@ falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, co
     if (n < 1 || n >= (1ll << 31)) return fail(FALCON_ERR_INVALID_ARG, "n must be in [1, 2^31)");
     if (m < 0 || m >= (1ll << 32)) return fail(FALCON_ERR_INVALID_ARG, "m must be in [0, 2^32)");
     if (!row_off || (m > 0 && !col)) return fail(FALCON_ERR_INVALID_ARG, "row_off/col is NULL");
-    if (opts && (opts->flags & ~(uint32_t)FALCON_LOAD_BUILD_COO))
+    if (opts && (opts->flags & ~(uint32_t)(FALCON_LOAD_BUILD_COO | FALCON_LOAD_BUILD_REVERSE)))
         return fail(FALCON_ERR_UNSUPPORTED, "unknown load flags 0x%x", opts->flags);
     falcon_graph *g = new (std::nothrow) falcon_graph();
     if (!g) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");

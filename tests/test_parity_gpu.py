@@ -153,6 +153,22 @@ def test_parity_worklist_noq(gpu_lib, name, dense_div, wl_noq, persist):
         assert np.array_equal(out, exp), f"{name}/{algo}/dd={dense_div}/noq={wl_noq}: {np.flatnonzero(out != exp)[:10]}"
 
 
+def test_load_flags_eager_layouts(gpu_lib):
+    """FALCON_LOAD_BUILD_COO / _REVERSE build the derived layouts at load;
+    results are the same as with the lazy builds; unknown flags are rejected."""
+    G = _graph("rmat-s")
+    g = gpu_lib.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0,
+                               flags=gpu_lib.LOAD_BUILD_COO | gpu_lib.LOAD_BUILD_REVERSE)
+    for algo in ALGOS:
+        exp = _oracle(algo, G.row_off, G.col, G.w, G.source)
+        for style in STYLES:
+            out, _ = _run(gpu_lib, g, algo, style, G.source)
+            assert np.array_equal(out, exp)
+    with pytest.raises(gpu_lib.FalconError) as e:
+        gpu_lib.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, flags=0x80)
+    assert e.value.name == "UNSUPPORTED"
+
+
 def test_memory_cache_reuse_and_trim(gpu_lib):
     """graph_free returns device memory to the library's cache; a second graph
     of the same shape reuses it; falcon_trim_memory hands it back."""
