@@ -256,7 +256,9 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  * blocked layout); they are rebuilt on the next call.
  *   "exchange"     partitioned graphs: boundary exchange per superstep, 0 = auto
  *                  (sparse pairs when smaller than the dense reduce-scatter),
- *                  1 = dense, 2 = sparse (env FALCON_EXCHANGE)
+ *                  1 = dense, 2 = sparse, 3 = fused (relax kernels write remote
+ *                  targets into their owners' arrays over peer memory; NCCL
+ *                  ranks map each other's arrays with CUDA IPC) (env FALCON_EXCHANGE)
  *   "wl_noq"       WORKLIST dense rounds mark the next bitmap without claims
  *                  or a queue (default 1, env FALCON_WL_NOQ; 0 = off)
  * Errors: INVALID_ARG (g/name NULL, value out of range), UNSUPPORTED (unknown

@@ -207,7 +207,10 @@ struct falcon_graph {
     unsigned long long *xpairs_d = nullptr;   // (simulated) pairs packed by sparse rounds of the current call
     uint2 **d_outboxes = nullptr;
     uint32_t **d_counts = nullptr;
-    uint32_t exchange = 0;                // 0 auto, 1 dense, 2 sparse (FALCON_EXCHANGE / option "exchange")
+    uint32_t exchange = 0;                // 0 auto, 1 dense, 2 sparse, 3 fused (FALCON_EXCHANGE / option "exchange")
+    int32_t **d_peer_val = nullptr;       // (partitioned, fused) every part's value array / bitmaps
+    uint32_t **d_peer_bm = nullptr;
+    std::vector<void *> ipc_opened;       // (NCCL, fused) peer mappings to close
     uint64_t xbytes = 0;                  // bytes moved by the exchanges of the last call (all ranks' share here)
 
     Args args() const {
@@ -1244,7 +1247,7 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
         } else if (!strcmp(name, "block_div")) {
             t->blk_div = (uint32_t)value;
         } else if (!strcmp(name, "exchange")) {
-            if (value > 2) return fail(FALCON_ERR_INVALID_ARG, "exchange: 0 auto, 1 dense, 2 sparse");
+            if (value > 3) return fail(FALCON_ERR_INVALID_ARG, "exchange: 0 auto, 1 dense, 2 sparse, 3 fused");
             g->exchange = (uint32_t)value;
         } else if (!strcmp(name, "wl_noq")) {
             t->wl_noq = (uint32_t)(value != 0);

@@ -35,7 +35,9 @@ __device__ int fk_probe_mode;   // tools/expand_probe.cu only (never defined in 
 constexpr unsigned FULL = 0xffffffffu;
 
 enum Algo : int { SSSP = 0, BFS = 1, CC = 2 };
-enum Style : int { VERTEX = 0, EDGE = 1, WORKLIST = 2, DELTA = 3 };
+enum Style : int { VERTEX = 0, EDGE = 1, WORKLIST = 2, DELTA = 3,
+                   VFUSED = 4 /* partitioned VERTEX rounds writing remote targets into their owners (partition.cuh) */ };
+__host__ __device__ constexpr bool is_vertex(int style) { return style == VERTEX || style == VFUSED; }
 enum DeltaMode : uint32_t { MODE_NEAR = 0, MODE_SCAN = 1 };
 enum DevStatus : int { ST_OK = 0, ST_OVERFLOW = 5, ST_NOT_CONVERGED = 6 };
 
@@ -98,6 +100,12 @@ struct Args {
     uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
     uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
+    // fused partitioned rounds (VFUSED): owned range, part bounds and the
+    // owners' value arrays / round bitmaps (peer memory on real GPUs)
+    uint32_t lo, hi, nparts;
+    const uint32_t *bounds;
+    int32_t *const *peer_val;
+    uint32_t *const *peer_bm;
     uint32_t delta_adapt;      // DELTA: adapt the bucket width per bucket (auto Δ)
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
@@ -491,6 +499,45 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
         return;
     }
 #endif
+    if constexpr (STYLE == VFUSED) {
+        // Fused partitioned round (SURVEY §8(e) stretch): a target owned by
+        // another part is gathered from, lowered in and marked in THAT part's
+        // value array and round bitmap -- through peer memory on real GPUs --
+        // so no exchange step follows the relax.
+        static_assert(ALGO == SSSP, "fused rounds run SSSP (BFS as unit-weight SSSP)");
+        int32_t *tv[U];
+        uint32_t *tb[U];
+        int32_t cur[U];
+        const size_t boff = (size_t)(x.bm_now - a.bm0);   // this round's bitmap inside every part's bitmaps
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            tv[q] = a.val; tb[q] = x.bm_now; cur[q] = 0;
+            if (!s.ok[q]) continue;
+            const uint32_t v = s.v[q];
+            if (v < a.lo || v >= a.hi) {
+                int lo = 0, hi = (int)a.nparts;   // owner: largest o with bounds[o] <= v
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (a.bounds[mid] <= v) lo = mid; else hi = mid;
+                }
+                tv[q] = a.peer_val[lo];
+                tb[q] = a.peer_bm[lo] + boff;
+            }
+            cur[q] = __ldcg(tv[q] + v);
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            if (!s.ok[q]) continue;
+            const uint32_t cand = s.p[q] + (uint32_t)s.wt[q];
+            if (cand >= (uint32_t)INF) { acc.ovf = true; continue; }
+            if ((int32_t)cand < cur[q]) {
+                atomicMin(tv[q] + s.v[q], (int32_t)cand);
+                atomicOr(tb[q] + (s.v[q] >> 5), 1u << (s.v[q] & 31));
+                acc.nu++; acc.chg = true;
+            }
+        }
+        return;
+    }
     int32_t cur[U];
 #pragma unroll
     for (int q = 0; q < U; q++) {
@@ -692,7 +739,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                     item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
                     if (u != NONE && first) {
                         acc.nv++;
-                        if (ALGO == BFS && STYLE == VERTEX) a.val[u] = (int32_t)x.lev;   // discovered last round
+                        if (ALGO == BFS && is_vertex(STYLE)) a.val[u] = (int32_t)x.lev;   // discovered last round
                     }
                     if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
                     relax_tile<ALGO, STYLE, U, COHERENT, NOQ>(a, x, beg, deg, pay, acc, pend);
@@ -746,10 +793,10 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
 // One round per launch (VERTEX, and the queue styles when not persistent).
 template <int ALGO, int STYLE, int B, int U, int MINB>
 __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
-    static_assert(STYLE == VERTEX || STYLE == WORKLIST || STYLE == DELTA, "expand is for VERTEX/WORKLIST/DELTA");
+    static_assert(is_vertex(STYLE) || STYLE == WORKLIST || STYLE == DELTA, "expand is for VERTEX/WORKLIST/DELTA");
     constexpr int WQ = (STYLE == WORKLIST || STYLE == DELTA) ? 256 : 1;
     Ctrl *c = a.ctrl;
-    if (c->done || (ALGO == BFS && STYLE == VERTEX && c->pull)) return;
+    if (c->done || (ALGO == BFS && is_vertex(STYLE) && c->pull)) return;
     if (STYLE == DELTA && c->mode != MODE_NEAR) {   // this round refills the near queue from the far set
         unsigned long long nv = 0;
         scan_far_round<false>(a, c, c->iter, c->thr, c->sel ? a.fr0 : a.fr1, nv);
@@ -757,13 +804,13 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         return;
     }
     const uint32_t iter = c->iter;
-    if (STYLE == VERTEX) clear_next_bitmap(a, iter);
+    if (is_vertex(STYLE)) clear_next_bitmap(a, iter);
     const uint32_t thr = STYLE == DELTA ? c->thr : 0xffffffffu;
     const uint32_t *in = c->sel ? a.fr1 : a.fr0;
     uint32_t *out = c->sel ? a.fr0 : a.fr1;
     const uint32_t nitems = c->in_len;
-    const bool dense = STYLE == VERTEX || (a.dense_div && nitems > a.n / a.dense_div);
-    const bool blocked = STYLE == VERTEX ? c->blk != 0 : (a.blk_div && nitems > a.n / a.blk_div);
+    const bool dense = is_vertex(STYLE) || (a.dense_div && nitems > a.n / a.dense_div);
+    const bool blocked = is_vertex(STYLE) ? c->blk != 0 : (a.blk_div && nitems > a.n / a.blk_div);
     __shared__ uint32_t s_q[B / 32][WQ];
     __shared__ uint32_t s_it[B / 32][1024];
     RoundAcc acc;

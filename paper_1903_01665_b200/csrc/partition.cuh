@@ -53,6 +53,7 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -69,7 +70,7 @@ NcclApi *nccl_api() {
     if (!api.h) return nullptr;
 #define SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))
     SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(Reduce); SYM(AllReduce);
-    SYM(Broadcast); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString); SYM(Send); SYM(Recv);
+    SYM(Broadcast); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString); SYM(Send); SYM(Recv); SYM(AllGather);
 #undef SYM
     if (!api.GetUniqueId || !api.CommInitRank || !api.Reduce || !api.AllReduce || !api.Broadcast ||
         !api.GroupStart || !api.GroupEnd) {
@@ -273,10 +274,14 @@ void destroy_partitioned(falcon_graph *g) {
     g->parts.clear();
     dfree(g->bounds_d); dfree(g->d_outboxes); dfree(g->d_counts); dfree(g->xpairs_d);
     g->bounds_d = nullptr; g->d_outboxes = nullptr; g->d_counts = nullptr; g->xpairs_d = nullptr;
+    for (void *q : g->ipc_opened) cudaIpcCloseMemHandle(q);
+    g->ipc_opened.clear();
+    dfree(g->d_peer_val); dfree(g->d_peer_bm);
+    g->d_peer_val = nullptr; g->d_peer_bm = nullptr;
 }
 
-// Buffers of the sparse exchange, allocated on first use.
-falcon_status_t ensure_sparse(falcon_graph *g) {
+// The part bounds on the device (sparse and fused exchanges).
+falcon_status_t ensure_bounds(falcon_graph *g) {
     if (g->bounds_d) return FALCON_OK;
     falcon_comm *cm = g->comm;
     const int P = cm->simulated ? cm->simulated : cm->nranks;
@@ -285,7 +290,71 @@ falcon_status_t ensure_sparse(falcon_graph *g) {
     for (int q = 0; q <= P; q++) hb[(size_t)q] = (uint32_t)g->bounds[(size_t)q];
     CU(dmalloc(&g->bounds_d, (size_t)P + 1));
     CU(dmalloc(&g->xpairs_d, 1));
+    CU(cudaMemsetAsync(g->xpairs_d, 0, 8, s));   // cached blocks are not zeroed
     CU(cudaMemcpyAsync(g->bounds_d, hb.data(), (size_t)(P + 1) * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    return FALCON_OK;
+}
+
+// Peer tables of the fused exchange: every part's value array and round
+// bitmaps.  Simulated parts: plain device pointers.  NCCL ranks: CUDA IPC
+// handles of each rank's arrays, all-gathered over NCCL and opened with
+// peer access (NVLink), so a relax kernel's atomicMin / atomicOr land
+// directly in the owner's memory.
+falcon_status_t ensure_fused(falcon_graph *g) {
+    if (g->d_peer_val) return FALCON_OK;
+    falcon_status_t st = ensure_bounds(g);
+    if (st != FALCON_OK) return st;
+    falcon_comm *cm = g->comm;
+    const int P = cm->simulated ? cm->simulated : cm->nranks;
+    cudaStream_t s = g->parts[0]->stream;
+    std::vector<int32_t *> hv((size_t)P);
+    std::vector<uint32_t *> hb((size_t)P);
+    if (cm->simulated) {
+        for (int q = 0; q < P; q++) { hv[(size_t)q] = g->parts[(size_t)q]->val; hb[(size_t)q] = g->parts[(size_t)q]->bm; }
+    } else {
+        NcclApi *nc = nccl_api();
+        if (!nc->AllGather) return fail(FALCON_ERR_COMM, "ncclAllGather unavailable");
+        falcon_graph *me = g->parts[0];
+        cudaIpcMemHandle_t mine[2];
+        CU(cudaIpcGetMemHandle(&mine[0], me->val));
+        CU(cudaIpcGetMemHandle(&mine[1], me->bm));
+        uint8_t *d_send = nullptr, *d_all = nullptr;
+        CU(dmalloc(&d_send, sizeof mine));
+        CU(dmalloc(&d_all, sizeof mine * (size_t)P));
+        CU(cudaMemcpyAsync(d_send, mine, sizeof mine, cudaMemcpyHostToDevice, s));
+        NC(nc->AllGather(d_send, d_all, sizeof mine, ncclUint8, cm->nccl, s));
+        std::vector<cudaIpcMemHandle_t> all((size_t)P * 2);
+        CU(cudaMemcpyAsync(all.data(), d_all, sizeof mine * (size_t)P, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        dfree(d_send); dfree(d_all);
+        for (int q = 0; q < P; q++) {
+            if (q == cm->rank) { hv[(size_t)q] = me->val; hb[(size_t)q] = me->bm; continue; }
+            void *pv = nullptr, *pb = nullptr;
+            CU(cudaIpcOpenMemHandle(&pv, all[(size_t)q * 2], cudaIpcMemLazyEnablePeerAccess));
+            CU(cudaIpcOpenMemHandle(&pb, all[(size_t)q * 2 + 1], cudaIpcMemLazyEnablePeerAccess));
+            g->ipc_opened.push_back(pv);
+            g->ipc_opened.push_back(pb);
+            hv[(size_t)q] = static_cast<int32_t *>(pv);
+            hb[(size_t)q] = static_cast<uint32_t *>(pb);
+        }
+    }
+    CU(dmalloc(&g->d_peer_val, (size_t)P));
+    CU(dmalloc(&g->d_peer_bm, (size_t)P));
+    CU(cudaMemcpyAsync(g->d_peer_val, hv.data(), sizeof(int32_t *) * P, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(g->d_peer_bm, hb.data(), sizeof(uint32_t *) * P, cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    return FALCON_OK;
+}
+
+// Buffers of the sparse exchange, allocated on first use.
+falcon_status_t ensure_sparse(falcon_graph *g) {
+    if (g->parts[0]->xcounts) return FALCON_OK;
+    falcon_status_t st0 = ensure_bounds(g);
+    if (st0 != FALCON_OK) return st0;
+    falcon_comm *cm = g->comm;
+    const int P = cm->simulated ? cm->simulated : cm->nranks;
+    cudaStream_t s = g->parts[0]->stream;
     std::vector<uint2 *> ho;
     std::vector<uint32_t *> hc;
     for (auto *p : g->parts) {
@@ -370,7 +439,7 @@ falcon_status_t load_partitioned(int64_t n, int64_t m, const uint32_t *row_off, 
     g->lo = cm->simulated ? 0 : g->bounds[cm->rank];
     g->hi = cm->simulated ? n : g->bounds[cm->rank + 1];
     g->stream = g->parts[0]->stream;
-    if (const char *ex = getenv("FALCON_EXCHANGE")) g->exchange = (uint32_t)atoi(ex) % 3u;
+    if (const char *ex = getenv("FALCON_EXCHANGE")) g->exchange = (uint32_t)atoi(ex) % 4u;
     return FALCON_OK;
 }
 
@@ -498,6 +567,16 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         CU(cudaMemcpyAsync(d_vals, hv.data(), sizeof(int32_t *) * P, cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(d_ctrls, hc.data(), sizeof(Ctrl *) * P, cudaMemcpyHostToDevice, s));
     }
+    const bool fused = g->exchange == 3 && algo != CC;
+    if (fused) {
+        falcon_status_t st = ensure_fused(g);
+        if (st != FALCON_OK) return st;
+        for (size_t i = 0; i < g->parts.size(); i++) {
+            falcon_graph *p = g->parts[i];
+            args[i].lo = (uint32_t)p->lo; args[i].hi = (uint32_t)p->hi; args[i].nparts = (uint32_t)P;
+            args[i].bounds = g->bounds_d; args[i].peer_val = g->d_peer_val; args[i].peer_bm = g->d_peer_bm;
+        }
+    }
     CU(cudaEventRecord(g->parts[0]->ev0, s));
     g->xbytes = 0;
     if (g->xpairs_d) CU(cudaMemsetAsync(g->xpairs_d, 0, 8, s));
@@ -517,6 +596,8 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
                 falcon_graph *p = g->parts[i];
                 if (algo == CC) {
                     launch_l2(p, k_cc_vertex<BLOCK>, p->grid_cc, s, args[i]);
+                } else if (fused) {   // remote targets land in their owners' arrays: no exchange step
+                    launch_l2(p, k_expand_warp<SSSP, VFUSED, BLOCK, 4, 3>, p->grid_expand_fr, s, args[i]);
                 } else {
                     launch_expand_warp<SSSP, VERTEX>(p, s, args[i]);
                 }
@@ -530,6 +611,8 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
                 }
                 for (size_t i = 0; i < g->parts.size(); i++)
                     launch_l2(g->parts[i], k_compress, g->parts[i]->grid_small, s, args[i]);
+            } else if (fused) {
+                // nothing to exchange: the relax kernels wrote into the owners
             } else {
                 // dense reduce-scatter or sparse (vertex, value) pairs, decided per round
                 bool sparse = false;

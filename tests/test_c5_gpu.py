@@ -51,7 +51,9 @@ def test_c5_partitioned_8_simulated(gpu_lib, name):
     comm = gpu_lib.falcon_comm_init_simulated(8)
     g = gpu_lib.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, comm=comm)
     out = np.empty(G.n, np.int32)
-    for algo in ("sssp", "bfs", "cc"):
-        gpu_lib.run(g, algo, "vertex", out, G.source)
-        assert np.array_equal(out, exp[algo]), f"{name}/P=8/{algo}: {np.flatnonzero(out != exp[algo])[:8]}"
+    for exchange in (0, 3):   # dense device reduce; fused peer writes
+        gpu_lib.falcon_set_option(g, "exchange", exchange)
+        for algo in ("sssp", "bfs", "cc"):
+            gpu_lib.run(g, algo, "vertex", out, G.source)
+            assert np.array_equal(out, exp[algo]), f"{name}/P=8/x{exchange}/{algo}: {np.flatnonzero(out != exp[algo])[:8]}"
     gpu_lib.graph_free(g)

@@ -38,10 +38,11 @@ def test_simulated_partition_parity(gpu_lib, name, P, algo):
 
 @pytest.mark.parametrize("name", GRAPHS)
 @pytest.mark.parametrize("P", [2, 3, 8])
-@pytest.mark.parametrize("exchange", [0, 1, 2])
+@pytest.mark.parametrize("exchange", [0, 1, 2, 3])
 def test_simulated_partition_exchange_modes(gpu_lib, name, P, exchange):
-    """Dense reduce-scatter, sparse (vertex, value) pairs, or the per-round
-    choice: the same fixpoint."""
+    """Dense reduce-scatter, sparse (vertex, value) pairs, the per-round
+    choice, or fused rounds whose relax kernels write remote targets straight
+    into their owners' arrays: the same fixpoint."""
     fb = gpu_lib
     G = _g(name)
     comm = fb.falcon_comm_init_simulated(P)
@@ -69,6 +70,9 @@ def test_sparse_exchange_moves_fewer_bytes(gpu_lib):
         moved[ex] = fb.graph_exchange_bytes(g)
     assert 0 < moved[2] < moved[1] / 10
     assert moved[0] == moved[1]   # simulated parts: auto keeps the dense device reduce
+    fb.falcon_set_option(g, "exchange", 3)   # fused: no exchange step at all
+    fb.run(g, "sssp", "vertex", out, G.source)
+    assert np.array_equal(out, oracle.run("sssp", G)) and fb.graph_exchange_bytes(g) == 0
 
 
 def test_simulated_partition_device_output_and_repeat(gpu_lib):

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -k "load_flags or load_validation" 2>&1 | tail -1
+timeout 1500 python -m pytest tests/test_partition_gpu.py tests/test_partition.py tests/test_c5_gpu.py -x -q 2>&1 | tail -2
