@@ -536,8 +536,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
                 acc.nu++; acc.chg = true;
             }
         }
-        return;
-    }
+    } else {
     int32_t cur[U];
 #pragma unroll
     for (int q = 0; q < U; q++) {
@@ -619,6 +618,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
             x.qn = 0;
         }
     }
+    }   // STYLE != VFUSED
 }
 
 // Relax the arcs of one 32-item tile (lane: value pay, arcs [beg, beg+deg)).
