@@ -128,6 +128,32 @@ void dfree(void *p) {
     c.live.erase(it);
 }
 
+// Pinned host copies of the control block: recycled through a free list, as
+// cudaFreeHost unregisters the page and can take tens to hundreds of ms on a
+// busy host (measured 16-515 ms per graph_free on this pool's boxes).
+struct HostCtrlCache {
+    std::mutex mu;
+    std::vector<void *> idle;
+};
+HostCtrlCache &host_ctrl_cache() {
+    static HostCtrlCache *c = new HostCtrlCache();
+    return *c;
+}
+cudaError_t host_ctrl_alloc(void **p, size_t bytes) {
+    HostCtrlCache &c = host_ctrl_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (!c.idle.empty()) { *p = c.idle.back(); c.idle.pop_back(); return cudaSuccess; }
+    }
+    return cudaMallocHost(p, bytes < 4096 ? 4096 : bytes);
+}
+void host_ctrl_free(void *p) {
+    if (!p) return;
+    HostCtrlCache &c = host_ctrl_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.idle.push_back(p);
+}
+
 template <typename T>
 cudaError_t dmalloc(T **p, size_t count) {
     return dev_alloc(reinterpret_cast<void **>(p), (count ? count : 1) * sizeof(T));
@@ -845,7 +871,7 @@ void destroy(falcon_graph *g) {
                     (void *)g->xcnt_recv, (void *)g->outbox, (void *)g->inbox, (void *)g->bounds_d,
                     (void *)g->d_outboxes, (void *)g->d_counts})
         dfree(p);   // back to the device cache (the stream was synchronised above)
-    if (g->h_ctrl) cudaFreeHost(g->h_ctrl);
+    host_ctrl_free(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
     if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
     delete g;
@@ -881,7 +907,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     CU(dmalloc(&g->tiles, (size_t)(MAX_BLK * ((uint64_t)n + 1) + 1023) / 1024 + 1));   // scan tile sums
     CU(dmalloc(&g->ctrl, 1));
     CU(dmalloc(&g->d_flags, 1));
-    CU(cudaMallocHost(&g->h_ctrl, sizeof(Ctrl)));
+    CU(host_ctrl_alloc(reinterpret_cast<void **>(&g->h_ctrl), sizeof(Ctrl)));
 
     CU(cudaMemcpyAsync(g->row_off, row_off, ((size_t)n + 1) * 4, cudaMemcpyDefault, s));
     if (m) CU(cudaMemcpyAsync(g->col, col, (size_t)m * 4, cudaMemcpyDefault, s));
@@ -1025,7 +1051,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     CU(dmalloc(&v->fr1, n + 1));
     CU(dmalloc(&v->ctrl, 1));
     CU(dmalloc(&v->cnt, 3 * (size_t)v->cnt_slots));
-    CU(cudaMallocHost(&v->h_ctrl, sizeof(Ctrl)));
+    CU(host_ctrl_alloc(reinterpret_cast<void **>(&v->h_ctrl), sizeof(Ctrl)));
     v->l2_window = p->l2_window;
     v->apw = p->apw;
     v->apw.base_ptr = v->val;
