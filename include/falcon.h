@@ -65,7 +65,7 @@ typedef enum {
     FALCON_ERR_NO_MEMORY = 3,     /* device allocation failed                                  */
     FALCON_ERR_CUDA = 4,          /* any other CUDA runtime error (graph may be unusable)      */
     FALCON_ERR_OVERFLOW = 5,      /* a finite distance would reach FALCON_INF                  */
-    FALCON_ERR_NOT_CONVERGED = 6, /* iteration cap (n + 2 rounds) exceeded                     */
+    FALCON_ERR_NOT_CONVERGED = 6, /* iteration cap (n + 2 rounds; DELTA 2n + 4) exceeded        */
     FALCON_ERR_COMM = 7,          /* reserved: multi-GPU communication failure                 */
     FALCON_ERR_UNSUPPORTED = 8    /* option not supported by this build                        */
 } falcon_status_t;
@@ -261,6 +261,17 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *                  ranks map each other's arrays with CUDA IPC) (env FALCON_EXCHANGE)
  *   "wl_noq"       WORKLIST dense rounds mark the next bitmap without claims
  *                  or a queue (default 1, env FALCON_WL_NOQ; 0 = off)
+ *   "local"        SSSP DELTA sparse rounds: each warp expands the in-bucket
+ *                  targets it improved itself, up to this many 32-item tiles
+ *                  per round, before handing the rest to the next round's
+ *                  queue (env FALCON_LOCAL; 0 = off; default set at load:
+ *                  16 when m < 3n, else 4).  Any relaxation order reaches the
+ *                  same fixpoint.
+ *   "local_max"    ... only in rounds of at most this many items (env
+ *                  FALCON_LOCAL_MAX; default unbounded when m < 3n, else 16384)
+ *   "bfs_unit"     BFS WORKLIST runs as unit-weight Δ-stepping with local
+ *                  continuation (same levels): -1 auto (m < 3n and local on;
+ *                  the default), 0 off, 1 on (env FALCON_BFS_UNIT)
  * Errors: INVALID_ARG (g/name NULL, value out of range), UNSUPPORTED (unknown
  * name; block_bytes of a graph that has, or is, a view). */
 FALCON_API falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t value);

@@ -179,6 +179,14 @@ struct falcon_graph {
     uint32_t dense_div = 32;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV; swept 8-128)
     uint32_t blk_div = 8;                // blocked round: frontier > n / blk_div (FALCON_BLOCK_DIV)
     uint32_t wl_noq = 1;                 // WORKLIST dense rounds without claims / queue (FALCON_WL_NOQ)
+    // SSSP DELTA sparse rounds: local continuation tiles per warp, in rounds of
+    // at most local_max items (FALCON_LOCAL / FALCON_LOCAL_MAX; set at load:
+    // 16 / unbounded on sparse high-diameter graphs (m < 3n), else 4 / 16384 --
+    // tools/survey.py sweep, profiles/r01_local.log)
+    uint32_t local_tiles = 4;
+    uint32_t local_max = 16384;
+    int32_t bfs_unit = -1;               // BFS WORKLIST as unit-weight Δ-stepping: -1 auto (m < 3n), 0 off, 1 on
+    bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     int32_t *val = nullptr;
@@ -242,9 +250,9 @@ struct falcon_graph {
     Args args() const {
         Args a{};
         a.n = (uint32_t)n; a.m = (uint32_t)m; a.nwords = nwords;
-        a.row_off = row_off; a.col = col; a.w = w; a.cw = use_unit ? cw_unit : cw; a.src = src;
+        a.row_off = row_off; a.col = col; a.w = w; a.cw = use_unit || unit_run ? cw_unit : cw; a.src = src;
         a.rin_off = rin_off; a.rin_col = rin_col;
-        const bool blk = rowb && !use_unit;
+        const bool blk = rowb && !use_unit && !unit_run;
         a.nblk = blk ? nblk : 1u;
         a.rowb = blk ? rowb : row_off;
         a.cwb = blk ? cwb : a.cw;
@@ -254,7 +262,9 @@ struct falcon_graph {
         a.dense_div = dense_div;
         a.blk_div = blk_div;
         a.wl_noq = wl_noq;
-        a.delta_adapt = delta == 0 ? 1u : 0u;   // auto Δ adapts per bucket; an explicit Δ is kept
+        a.local_tiles = local_tiles;
+        a.local_max = local_max;
+        a.delta_adapt = delta == 0 || unit_run ? 1u : 0u;   // auto Δ adapts per bucket; an explicit Δ is kept
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
@@ -398,6 +408,7 @@ int launch_round(falcon_graph *g, int algo, int style, cudaStream_t s, cudaGraph
     R(SSSP, VERTEX) R(SSSP, EDGE) R(SSSP, WORKLIST) R(SSSP, DELTA)
     R(BFS, VERTEX) R(BFS, EDGE) R(BFS, WORKLIST)
 #undef R
+    if (algo == BFS && style == DELTA) return Round<SSSP, DELTA>::launch(g, s, h, in_graph, tr);   // unit-weight BFS
     return 0;
 }
 
@@ -584,12 +595,40 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
     if (style == DELTA && algo != SSSP) return fail(FALCON_ERR_INVALID_ARG, "FALCON_STYLE_DELTA is an SSSP schedule");
     if (algo != CC && (int64_t)source >= g->n) return fail(FALCON_ERR_INVALID_ARG, "source %u >= n", source);
     CU(cudaSetDevice(g->device));
+    // BFS WORKLIST on a sparse high-diameter graph runs as unit-weight
+    // Δ-stepping with local continuation (R19): the hop
+    // distance is the least fixpoint of MIN-relaxation with w = 1, whatever
+    // the order.  The kernels are SSSP's over a (col, 1) copy of the arcs
+    // (built on first use, 8 bytes per arc); the CUDA graph is cached in the
+    // (BFS, DELTA) slot.  A view uses its parent's copy when there is one.
+    falcon_graph *root = g->parent ? g->parent : g;
+    const bool unit = algo == BFS && style == WORKLIST &&
+                      (g->bfs_unit > 0 || (g->bfs_unit < 0 && g->local_tiles && g->m < 3 * g->n)) &&
+                      (!g->parent || root->cw_unit);
+    g->unit_run = unit;
+    if (unit) {
+        style = DELTA;
+        if (!root->cw_unit) {   // (only the root builds it; published once complete)
+            uint2 *cu = nullptr;
+            CU(dmalloc(&cu, (size_t)(g->m ? g->m : 1)));
+            if (g->m) {
+                int32_t *ones = nullptr;
+                CU(dmalloc(&ones, (size_t)g->m));
+                k_fill_i32<<<g->num_sms * 8, BLOCK, 0, g->stream>>>(ones, (uint64_t)g->m, 1);
+                k_interleave<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint64_t)g->m, g->col, ones, cu);
+                CU(cudaStreamSynchronize(g->stream));
+                dfree(ones);
+            }
+            root->cw_unit = cu;
+        }
+        g->cw_unit = root->cw_unit;
+    }
     if (!g->parent) {   // a view shares layouts its parent built in graph_share
         if (style == EDGE) {
             falcon_status_t st = ensure_src(g);
             if (st != FALCON_OK) return st;
         }
-        if (algo == SSSP) {
+        if (algo == SSSP && !unit) {
             falcon_status_t st = ensure_blocked(g);
             if (st != FALCON_OK) return st;
         }
@@ -600,9 +639,11 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
     }
     cudaStream_t s = g->stream;
     Args a = g->args();
-    const uint32_t cap = (uint32_t)(g->n + 2 > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : g->n + 2);
+    // round cap (R11): n + 2 (Bellman-Ford); DELTA adds one refill round per bucket
+    const int64_t capn = style == DELTA ? 2 * g->n + 4 : g->n + 2;
+    const uint32_t cap = (uint32_t)(capn > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : capn);
     uint32_t delta = 1;
-    if (style == DELTA) {
+    if (style == DELTA && !unit) {
         if (g->delta > 0) {
             delta = (uint32_t)g->delta;
         } else {
@@ -621,7 +662,7 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
         }
     }
     CU(cudaEventRecord(g->ev0, s));
-    if (algo == SSSP) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
+    if (algo == SSSP || unit) k_init<SSSP><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
     else if (algo == BFS) k_init<BFS><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
     else k_init<CC><<<g->grid_small, BLOCK, 0, s>>>(a, source, cap, 3u * g->cnt_slots, style, delta);
     CU(cudaGetLastError());
@@ -763,6 +804,7 @@ falcon_status_t run_mst(falcon_graph *g, int style, int64_t *total, int64_t *ned
         return fail(FALCON_ERR_UNSUPPORTED, "falcon_mst runs VERTEX or EDGE style (Borůvka is arc-parallel)");
     if (g->pend_algo >= 0) return fail(FALCON_ERR_INVALID_ARG, "a call is already in flight on this graph");
     CU(cudaSetDevice(g->device));
+    g->unit_run = false;
     if (!g->parent) {
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
@@ -851,7 +893,7 @@ void destroy(falcon_graph *g) {
     if (g->parent) {   // a view: the arrays below belong to the parent
         g->parent->nviews--;
         g->row_off = g->col = g->src = g->rowb = g->srcb = g->rin_off = g->rin_col = g->tiles = nullptr;
-        g->w = nullptr; g->cw = g->cwb = g->chunk = g->chunkb = g->chunks = nullptr;
+        g->w = nullptr; g->cw = g->cwb = g->chunk = g->chunkb = g->chunks = g->cw_unit = nullptr;
         g->d_flags = nullptr;
     }
     for (auto &row : g->execs)
@@ -869,7 +911,7 @@ void destroy(falcon_graph *g) {
                     (void *)g->fr0, (void *)g->fr1, (void *)g->tiles, (void *)g->ctrl, (void *)g->cnt,
                     (void *)g->d_flags, (void *)g->mst_best, (void *)g->mst_list, (void *)g->xcounts,
                     (void *)g->xcnt_recv, (void *)g->outbox, (void *)g->inbox, (void *)g->bounds_d,
-                    (void *)g->d_outboxes, (void *)g->d_counts})
+                    (void *)g->d_outboxes, (void *)g->d_counts, (void *)g->cw_unit})
         dfree(p);   // back to the device cache (the stream was synchronised above)
     host_ctrl_free(g->h_ctrl);
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -950,6 +992,10 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (const char *bmb = getenv("FALCON_BLOCK_MB")) g->blk_bytes = (size_t)atoll(bmb) << 20;   // 0: no blocking
     if (const char *dd = getenv("FALCON_DENSE_DIV")) g->dense_div = (uint32_t)atoi(dd);        // 0: never dense
     if (const char *wq = getenv("FALCON_WL_NOQ")) g->wl_noq = (uint32_t)atoi(wq);
+    if (m < 3 * n) { g->local_tiles = 16; g->local_max = 0xffffffffu; }
+    if (const char *lt = getenv("FALCON_LOCAL")) g->local_tiles = (uint32_t)atoi(lt);
+    if (const char *lm = getenv("FALCON_LOCAL_MAX")) g->local_max = (uint32_t)atoll(lm);
+    if (const char *bu = getenv("FALCON_BFS_UNIT")) g->bfs_unit = (int32_t)atoi(bu);
     if (const char *bd = getenv("FALCON_BLOCK_DIV")) g->blk_div = (uint32_t)atoi(bd);          // 0: never blocked
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
@@ -1026,7 +1072,8 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->rowb = p->rowb; v->srcb = p->srcb; v->cwb = p->cwb;
     v->chunk = p->chunk; v->chunkb = p->chunkb; v->chunks = p->chunks;
     v->nblk = p->nblk; v->bsz = p->bsz; v->blk_bytes = p->blk_bytes;
-    v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq;
+    v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
+    v->bfs_unit = p->bfs_unit;
     v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
     v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
@@ -1257,7 +1304,8 @@ falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta) {
 
 falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t value) {
     if (!g || !name) return fail(FALCON_ERR_INVALID_ARG, "graph or option name is NULL");
-    if (value < 0 || value > 0xffffffffll) return fail(FALCON_ERR_INVALID_ARG, "option value out of range");
+    if ((value < 0 && !(value == -1 && !strcmp(name, "bfs_unit"))) || value > 0xffffffffll)
+        return fail(FALCON_ERR_INVALID_ARG, "option value out of range");
     std::vector<falcon_graph *> targets;
     if (g->comm) targets = g->parts; else targets.push_back(g);
     for (falcon_graph *t : targets) {
@@ -1277,6 +1325,13 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             g->exchange = (uint32_t)value;
         } else if (!strcmp(name, "wl_noq")) {
             t->wl_noq = (uint32_t)(value != 0);
+        } else if (!strcmp(name, "local")) {
+            t->local_tiles = (uint32_t)value;
+        } else if (!strcmp(name, "bfs_unit")) {
+            if (value < -1 || value > 1) return fail(FALCON_ERR_INVALID_ARG, "bfs_unit: -1 auto, 0 off, 1 on");
+            t->bfs_unit = (int32_t)value;
+        } else if (!strcmp(name, "local_max")) {
+            t->local_max = (uint32_t)std::min<int64_t>(value, 0xffffffffll);
         } else if (!strcmp(name, "pull_div")) {
             t->pull_div = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {

@@ -107,6 +107,8 @@ struct Args {
     int32_t *const *peer_val;
     uint32_t *const *peer_bm;
     uint32_t delta_adapt;      // DELTA: adapt the bucket width per bucket (auto Δ)
+    uint32_t local_tiles;      // SSSP sparse queue rounds: local continuation tiles per warp (0 = off)
+    uint32_t local_max;        // ... in rounds of at most local_max items
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
@@ -456,9 +458,33 @@ struct Xw {
     const uint2 *arcs;      // (col, w) words (SSSP)
     uint32_t *bm_now, *bm_prev, *out, *wq;
     Ctrl *c;
-    uint32_t lev, thr, qn, pend_min;
+    uint32_t lev, thr, qh, qn, pend_min;   // wq[qh, qn): staged appends / the local stack (LOCAL)
     uint64_t pf, pl;
 };
+
+// Local continuation (LOCAL rounds): hand the warp's unexpanded local items
+// wq[qh, qn) over to the next round -- claim each in this round's bitmap and
+// append the newly claimed ones to the queue.
+__device__ __forceinline__ void spill_local(Xw &x) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i0 = x.qh; i0 < x.qn; i0 += 32) {   // warp-uniform
+        const uint32_t i = i0 + lane;
+        uint32_t v = 0;
+        bool want = false;
+        if (i < x.qn) {
+            v = x.wq[i];
+            want = !(atomicOr(x.bm_now + (v >> 5), 1u << (v & 31)) & (1u << (v & 31)));
+        }
+        const unsigned mask = __ballot_sync(FULL, want);
+        if (!mask) continue;
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&x.c->out_len, (uint32_t)__popc(mask));
+        b = __shfl_sync(FULL, b, 0);
+        if (want) x.out[b + __popc(mask & ((1u << lane) - 1u))] = v;
+    }
+    __syncwarp();
+    x.qh = x.qn = 0;
+}
 
 template <int ALGO, bool COHERENT>
 __device__ __forceinline__ void item_rows(const Args &a, const Xw &x, uint32_t u, uint32_t &pay, uint32_t &beg,
@@ -483,7 +509,10 @@ struct Step {
 // Gather the targets' values of a loaded step and relax its arcs.  NOQ: a
 // dense WORKLIST round marks improved vertices like VERTEX does (reductions,
 // no claim, no queue append): its successor reads the frontier from the bitmap.
-template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false>
+// LOCAL: an improved in-bucket target is pushed unclaimed onto the warp's
+// local stack wq[qh, qn) (FIFO), which the warp expands itself later in the
+// round (expand_round); what it leaves over is claimed and queued then.
+template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false, bool LOCAL = false>
 __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &s, RoundAcc &acc) {
     constexpr bool QUEUE = (STYLE == WORKLIST || STYLE == DELTA) && !NOQ;
     constexpr int WQ = QUEUE ? 256 : 1;
@@ -587,6 +616,29 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
             for (int q = 0; q < U; q++)
                 if (need[q]) atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
         }
+    } else if (LOCAL) {
+        static_assert(!LOCAL || ALGO == SSSP, "local continuation is min-relaxation (SSSP)");
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const unsigned mask = __ballot_sync(FULL, need[q]);
+            if (need[q]) x.wq[x.qn + __popc(mask & ((1u << lane) - 1u))] = citem[q];
+            x.qn += __popc(mask);
+        }
+        __syncwarp();
+        if (x.qn > (uint32_t)(WQ - 32 * U)) {   // room for the next step: compact, else hand everything over
+            const uint32_t cnt = x.qn - x.qh;
+            if (x.qh >= 32 * U) {
+                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {   // ascending chunks: writes stay below later reads
+                    const uint32_t t = i0 + lane < cnt ? x.wq[x.qh + i0 + lane] : 0u;
+                    __syncwarp();
+                    if (i0 + lane < cnt) x.wq[i0 + lane] = t;
+                    __syncwarp();
+                }
+                x.qh = 0; x.qn = cnt;
+            } else {
+                spill_local(x);
+            }
+        }
     } else {
         uint32_t got[U];
 #pragma unroll
@@ -629,7 +681,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
 // ncu: 43 % of the stall samples); here the arc loads of tile t are in flight
 // while tile t-1's gathers are waited on.  The caller drains `pend` with
 // relax_step at the end of the round.
-template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ>
+template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ, bool LOCAL = false>
 __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, uint32_t deg, uint32_t pay,
                                            RoundAcc &acc, Step<U> &pend) {
     const int lane = threadIdx.x & 31;
@@ -671,7 +723,7 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
                 }
             }
         }
-        if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ>(a, x, pend, acc);
+        if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ, LOCAL>(a, x, pend, acc);
         pend = nx;
         pend.live = true;
     }
@@ -679,7 +731,7 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
 
 // One round of expansion by this warp.  sit: the warp's 1024-entry shared
 // item list (dense rounds).
-template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false>
+template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false, bool LOCAL = false>
 __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, const uint32_t *in,
                                              uint32_t *out, uint32_t nitems, bool dense, bool blocked, uint32_t *wq,
                                              uint32_t *sit, RoundAcc &acc) {
@@ -689,7 +741,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
     const uint32_t wstride = nwarps * 32;
     Xw x;
     x.bm_now = bm_of(a, iter); x.bm_prev = bm_of(a, iter - 1); x.out = out; x.wq = wq; x.c = c;
-    x.lev = iter - 1; x.thr = thr; x.qn = 0; x.pend_min = 0xffffffffu;
+    x.lev = iter - 1; x.thr = thr; x.qh = 0; x.qn = 0; x.pend_min = 0xffffffffu;
     x.pf = pol_evict_first(); x.pl = pol_evict_last();
     blocked = blocked && ALGO == SSSP && a.nblk > 1;
     const uint32_t K = blocked ? a.nblk : 1u;
@@ -763,12 +815,38 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                 if (QUEUE && last && u != NONE) x.bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
                 if (u != NONE && first) acc.nv++;
                 if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
-                relax_tile<ALGO, STYLE, U, COHERENT, NOQ>(a, x, beg, deg, pay, acc, pend);
+                relax_tile<ALGO, STYLE, U, COHERENT, NOQ, LOCAL>(a, x, beg, deg, pay, acc, pend);
             }
         }
     }
-    if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ>(a, x, pend, acc);   // drain the pipeline
-    if (QUEUE && !NOQ) {
+    if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ, LOCAL>(a, x, pend, acc);   // drain the pipeline
+    if constexpr (LOCAL) {
+        // Local continuation: the warp expands the targets it improved itself,
+        // 32 at a time, up to local_tiles tiles, instead of leaving each hop to
+        // a round of its own (road graphs: thousands of rounds of a few
+        // thousand items, each round bound by launch and dependent-access
+        // latency).  Any relaxation order reaches the same least fixpoint
+        // (R8); values written in this kernel are read L1-bypassing
+        // (COHERENT), so every expansion sees the value that pushed it or a
+        // lower one.
+        pend.live = false;
+        for (uint32_t t = 0; t < a.local_tiles && x.qn > x.qh; t++) {   // warp-uniform
+            const uint32_t take = min(x.qn - x.qh, 32u);
+            const uint32_t u = lane < take ? x.wq[x.qh + lane] : NONE;
+            __syncwarp();
+            x.qh += take;
+            uint32_t pay, beg, end;
+            item_rows<ALGO, true>(a, x, u, pay, beg, end);
+            uint32_t deg = end - beg;
+            if (u != NONE) acc.nv++;
+            if (u == NONE || pay == (uint32_t)INF) deg = 0;
+            relax_tile<ALGO, STYLE, U, true, NOQ, LOCAL>(a, x, beg, deg, pay, acc, pend);
+            if (pend.live) relax_step<ALGO, STYLE, U, true, NOQ, LOCAL>(a, x, pend, acc);
+            pend.live = false;
+        }
+        spill_local(x);
+    }
+    if (QUEUE && !NOQ && !LOCAL) {
         __syncwarp();
         if (x.qn) {
             uint32_t b = 0;
@@ -822,6 +900,10 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         if (blockIdx.x == 0 && threadIdx.x == 0) c->noq = 1;
         expand_round<ALGO, STYLE, U, false, true>(a, c, iter, thr, in, out, nitems, true, blocked,
                                                   s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
+    } else if (ALGO == SSSP && STYLE == DELTA && a.local_tiles && nitems <= a.local_max && !dense && !blocked) {
+        // Δ-stepping's light phase with local continuation (expand_round)
+        expand_round<ALGO, STYLE, U, false, false, ALGO == SSSP && STYLE == DELTA>(
+            a, c, iter, thr, in, out, nitems, false, false, s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
     } else {
         expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems,
                                             dense || (STYLE == WORKLIST && c->prevnoq), blocked,

@@ -153,6 +153,44 @@ def test_parity_worklist_noq(gpu_lib, name, dense_div, wl_noq, persist):
         assert np.array_equal(out, exp), f"{name}/{algo}/dd={dense_div}/noq={wl_noq}: {np.flatnonzero(out != exp)[:10]}"
 
 
+@pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s", "ragged", "tiny"])
+@pytest.mark.parametrize("local", [1, 2, 16, 1000])
+@pytest.mark.parametrize("dense_div", [32, 1])
+def test_parity_local_continuation(gpu_lib, name, local, dense_div):
+    """SSSP queue rounds whose warps expand the targets they improved
+    themselves (option `local`) reach the same fixpoint: small
+    budgets hand most local items back to the queue (claims), large ones
+    overflow the warp's stack (compaction / spill); Δ = 1 and Δ = 7 keep most
+    targets outside the bucket."""
+    G = _graph(name)
+    exp = oracle.sssp(G.row_off, G.col, G.w, G.source)
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    gpu_lib.falcon_set_option(g, "local", local)
+    gpu_lib.falcon_set_option(g, "dense_div", dense_div)
+    for delta in (0, 1, 7):
+        gpu_lib.falcon_set_delta(g, delta)
+        for style in ("worklist", "delta"):
+            for rep in range(2):
+                out, st = _run(gpu_lib, g, "sssp", style, G.source, device_out=rep == 1)
+                assert np.array_equal(out, exp), f"{name}/{style}/local={local}/Δ={delta}: {np.flatnonzero(out != exp)[:10]}"
+    exp_bfs = oracle.bfs(G.row_off, G.col, G.source)
+    for bfs_unit in (1, 0, -1):   # BFS WORKLIST as unit-weight Δ-stepping (R19): on, off, auto
+        gpu_lib.falcon_set_option(g, "bfs_unit", bfs_unit)
+        for rep in range(2):
+            out, st = _run(gpu_lib, g, "bfs", "worklist", G.source, device_out=rep == 1)
+            assert np.array_equal(out, exp_bfs), f"{name}/bfs/local={local}/unit={bfs_unit}: {np.flatnonzero(out != exp_bfs)[:10]}"
+            assert st.iterations >= 1
+    for style in ("vertex", "edge"):   # the options leave the other styles alone
+        out, _ = _run(gpu_lib, g, "bfs", style, G.source)
+        assert np.array_equal(out, exp_bfs)
+    out, _ = _run(gpu_lib, g, "cc", "worklist", G.source)
+    assert np.array_equal(out, oracle.cc(G.row_off, G.col))
+    tot, ne, _ = gpu_lib.falcon_mst(g, "vertex")   # after a unit-weight BFS: real weights again
+    assert (tot, ne) == oracle.mst(G.row_off, G.col, G.w)[:2]
+    out, _ = _run(gpu_lib, g, "sssp", "vertex", G.source)
+    assert np.array_equal(out, exp)
+
+
 def test_load_flags_eager_layouts(gpu_lib):
     """FALCON_LOAD_BUILD_COO / _REVERSE build the derived layouts at load;
     results are the same as with the lazy builds; unknown flags are rejected."""
@@ -195,6 +233,9 @@ def test_set_option_rejects_unknown(gpu_lib):
         gpu_lib.falcon_set_option(g, "no_such_option", 1)
     with pytest.raises(gpu_lib.FalconError):
         gpu_lib.falcon_set_option(g, "dense_div", -1)
+    for bad in (-2, 2):
+        with pytest.raises(gpu_lib.FalconError):
+            gpu_lib.falcon_set_option(g, "bfs_unit", bad)
 
 
 def test_delta_rejects_bfs_cc_and_negative(gpu_lib):

@@ -1,3 +1,7 @@
-python tools/e2e_timing.py > gpurun_out/e2e_timing.log 2>&1
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_concurrent_gpu.py -x -q -k "not full_config and not three" 2>&1 | tail -1 >> gpurun_out/e2e_timing.log
-timeout 600 python bench.py --steps 5 --no-cpu-baseline > gpurun_out/bench_e2e.log 2>&1
+# local continuation defaults + unit-weight BFS: parity, then timings
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/local4.log 2>&1
+timeout 1500 python -m pytest tests/test_parity_gpu.py tests/test_concurrent_gpu.py -x -q 2>&1 | tail -5 >> gpurun_out/local4.log
+echo "== defaults" >> gpurun_out/local4.log
+timeout 900 python tools/survey.py --configs grid-24M,rand-25M,rmat-10M --reps 3 2>&1 | grep -v "^==" >> gpurun_out/local4.log
+echo "== grid bfs unit LOCAL=64" >> gpurun_out/local4.log
+timeout 600 python tools/survey.py --configs grid-24M --algos bfs,sssp --styles worklist,delta --reps 3 --env FALCON_LOCAL=64 2>&1 | grep -v "^==" >> gpurun_out/local4.log
