@@ -265,10 +265,14 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *                  targets it improved itself, up to this many 32-item tiles
  *                  per round, before handing the rest to the next round's
  *                  queue (env FALCON_LOCAL; 0 = off; default set at load:
- *                  16 when m < 3n, else 4).  Any relaxation order reaches the
+ *                  16 when m < 3n, 4 when m < 6n, else 0).  Any relaxation order reaches the
  *                  same fixpoint.
  *   "local_max"    ... only in rounds of at most this many items (env
  *                  FALCON_LOCAL_MAX; default unbounded when m < 3n, else 16384)
+ *   "wl_local"     the same for SSSP WORKLIST sparse rounds (env FALCON_WL_LOCAL;
+ *                  default set at load: 4 when m < 3n, else 0 = off)
+ *   "wl_local_max" ... in rounds of at most this many items (env
+ *                  FALCON_WL_LOCAL_MAX; default 262144)
  *   "bfs_unit"     BFS WORKLIST runs as unit-weight Δ-stepping with local
  *                  continuation (same levels): -1 auto (m < 3n and local on;
  *                  the default), 0 off, 1 on (env FALCON_BFS_UNIT)

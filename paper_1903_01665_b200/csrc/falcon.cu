@@ -181,10 +181,15 @@ struct falcon_graph {
     uint32_t wl_noq = 1;                 // WORKLIST dense rounds without claims / queue (FALCON_WL_NOQ)
     // SSSP DELTA sparse rounds: local continuation tiles per warp, in rounds of
     // at most local_max items (FALCON_LOCAL / FALCON_LOCAL_MAX; set at load:
-    // 16 / unbounded on sparse high-diameter graphs (m < 3n), else 4 / 16384 --
+    // 16 / unbounded on sparse high-diameter graphs (m < 3n), 4 / 16384 below
+    // m = 6n, else off --
     // tools/survey.py sweep, profiles/r01_local.log)
     uint32_t local_tiles = 4;
     uint32_t local_max = 16384;
+    // ... SSSP WORKLIST (FALCON_WL_LOCAL / FALCON_WL_LOCAL_MAX; set at load:
+    // 4 tiles in rounds of <= 256 K items when m < 3n, else off)
+    uint32_t wl_local_tiles = 0;
+    uint32_t wl_local_max = 262144;
     int32_t bfs_unit = -1;               // BFS WORKLIST as unit-weight Δ-stepping: -1 auto (m < 3n), 0 off, 1 on
     bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
@@ -264,6 +269,8 @@ struct falcon_graph {
         a.wl_noq = wl_noq;
         a.local_tiles = local_tiles;
         a.local_max = local_max;
+        a.wl_local_tiles = wl_local_tiles;
+        a.wl_local_max = wl_local_max;
         a.delta_adapt = delta == 0 || unit_run ? 1u : 0u;   // auto Δ adapts per bucket; an explicit Δ is kept
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
@@ -992,7 +999,10 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (const char *bmb = getenv("FALCON_BLOCK_MB")) g->blk_bytes = (size_t)atoll(bmb) << 20;   // 0: no blocking
     if (const char *dd = getenv("FALCON_DENSE_DIV")) g->dense_div = (uint32_t)atoi(dd);        // 0: never dense
     if (const char *wq = getenv("FALCON_WL_NOQ")) g->wl_noq = (uint32_t)atoi(wq);
-    if (m < 3 * n) { g->local_tiles = 16; g->local_max = 0xffffffffu; }
+    if (m < 3 * n) { g->local_tiles = 16; g->local_max = 0xffffffffu; g->wl_local_tiles = 4; }
+    else if (m >= 6 * n) g->local_tiles = 0;   // dense / skewed (rmat): measured no gain
+    if (const char *lt = getenv("FALCON_WL_LOCAL")) g->wl_local_tiles = (uint32_t)atoi(lt);
+    if (const char *lm = getenv("FALCON_WL_LOCAL_MAX")) g->wl_local_max = (uint32_t)atoll(lm);
     if (const char *lt = getenv("FALCON_LOCAL")) g->local_tiles = (uint32_t)atoi(lt);
     if (const char *lm = getenv("FALCON_LOCAL_MAX")) g->local_max = (uint32_t)atoll(lm);
     if (const char *bu = getenv("FALCON_BFS_UNIT")) g->bfs_unit = (int32_t)atoi(bu);
@@ -1073,6 +1083,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->chunk = p->chunk; v->chunkb = p->chunkb; v->chunks = p->chunks;
     v->nblk = p->nblk; v->bsz = p->bsz; v->blk_bytes = p->blk_bytes;
     v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
+    v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max;
     v->bfs_unit = p->bfs_unit;
     v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
@@ -1332,6 +1343,10 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->bfs_unit = (int32_t)value;
         } else if (!strcmp(name, "local_max")) {
             t->local_max = (uint32_t)std::min<int64_t>(value, 0xffffffffll);
+        } else if (!strcmp(name, "wl_local")) {
+            t->wl_local_tiles = (uint32_t)value;
+        } else if (!strcmp(name, "wl_local_max")) {
+            t->wl_local_max = (uint32_t)std::min<int64_t>(value, 0xffffffffll);
         } else if (!strcmp(name, "pull_div")) {
             t->pull_div = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {

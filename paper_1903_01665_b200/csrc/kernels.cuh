@@ -107,8 +107,10 @@ struct Args {
     int32_t *const *peer_val;
     uint32_t *const *peer_bm;
     uint32_t delta_adapt;      // DELTA: adapt the bucket width per bucket (auto Δ)
-    uint32_t local_tiles;      // SSSP sparse queue rounds: local continuation tiles per warp (0 = off)
+    uint32_t local_tiles;      // SSSP DELTA sparse rounds: local continuation tiles per warp (0 = off)
     uint32_t local_max;        // ... in rounds of at most local_max items
+    uint32_t wl_local_tiles;   // the same for SSSP WORKLIST sparse rounds
+    uint32_t wl_local_max;
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
@@ -734,7 +736,7 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
 template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false, bool LOCAL = false>
 __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, const uint32_t *in,
                                              uint32_t *out, uint32_t nitems, bool dense, bool blocked, uint32_t *wq,
-                                             uint32_t *sit, RoundAcc &acc) {
+                                             uint32_t *sit, RoundAcc &acc, uint32_t ltiles = 0) {
     constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -822,7 +824,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
     if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ, LOCAL>(a, x, pend, acc);   // drain the pipeline
     if constexpr (LOCAL) {
         // Local continuation: the warp expands the targets it improved itself,
-        // 32 at a time, up to local_tiles tiles, instead of leaving each hop to
+        // 32 at a time, up to ltiles tiles, instead of leaving each hop to
         // a round of its own (road graphs: thousands of rounds of a few
         // thousand items, each round bound by launch and dependent-access
         // latency).  Any relaxation order reaches the same least fixpoint
@@ -830,7 +832,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
         // (COHERENT), so every expansion sees the value that pushed it or a
         // lower one.
         pend.live = false;
-        for (uint32_t t = 0; t < a.local_tiles && x.qn > x.qh; t++) {   // warp-uniform
+        for (uint32_t t = 0; t < ltiles && x.qn > x.qh; t++) {   // warp-uniform
             const uint32_t take = min(x.qn - x.qh, 32u);
             const uint32_t u = lane < take ? x.wq[x.qh + lane] : NONE;
             __syncwarp();
@@ -900,10 +902,13 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         if (blockIdx.x == 0 && threadIdx.x == 0) c->noq = 1;
         expand_round<ALGO, STYLE, U, false, true>(a, c, iter, thr, in, out, nitems, true, blocked,
                                                   s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
-    } else if (ALGO == SSSP && STYLE == DELTA && a.local_tiles && nitems <= a.local_max && !dense && !blocked) {
-        // Δ-stepping's light phase with local continuation (expand_round)
-        expand_round<ALGO, STYLE, U, false, false, ALGO == SSSP && STYLE == DELTA>(
-            a, c, iter, thr, in, out, nitems, false, false, s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
+    } else if (ALGO == SSSP && (STYLE == DELTA ? a.local_tiles && nitems <= a.local_max
+                                               : a.wl_local_tiles && nitems <= a.wl_local_max && !c->prevnoq) &&
+               !dense && !blocked) {
+        // sparse SSSP rounds with local continuation (expand_round)
+        expand_round<ALGO, STYLE, U, false, false, ALGO == SSSP>(
+            a, c, iter, thr, in, out, nitems, false, false, s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc,
+            STYLE == DELTA ? a.local_tiles : a.wl_local_tiles);
     } else {
         expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems,
                                             dense || (STYLE == WORKLIST && c->prevnoq), blocked,

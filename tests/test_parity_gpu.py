@@ -166,6 +166,8 @@ def test_parity_local_continuation(gpu_lib, name, local, dense_div):
     exp = oracle.sssp(G.row_off, G.col, G.w, G.source)
     g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
     gpu_lib.falcon_set_option(g, "local", local)
+    gpu_lib.falcon_set_option(g, "wl_local", local)
+    gpu_lib.falcon_set_option(g, "wl_local_max", 1 << 30)
     gpu_lib.falcon_set_option(g, "dense_div", dense_div)
     for delta in (0, 1, 7):
         gpu_lib.falcon_set_delta(g, delta)
