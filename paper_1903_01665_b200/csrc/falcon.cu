@@ -190,6 +190,7 @@ struct falcon_graph {
     // 4 tiles in rounds of <= 256 K items when m < 3n, else off)
     uint32_t wl_local_tiles = 0;
     uint32_t wl_local_max = 262144;
+    uint32_t delta_cap = 0;              // adaptive Δ growth cap x Δ0 (0 = 128; FALCON_DELTA_CAP)
     int32_t bfs_unit = -1;               // BFS WORKLIST as unit-weight Δ-stepping: -1 auto (m < 3n), 0 off, 1 on
     bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
@@ -271,6 +272,7 @@ struct falcon_graph {
         a.local_max = local_max;
         a.wl_local_tiles = wl_local_tiles;
         a.wl_local_max = wl_local_max;
+        a.delta_cap = delta_cap;
         a.delta_adapt = delta == 0 || unit_run ? 1u : 0u;   // auto Δ adapts per bucket; an explicit Δ is kept
         a.val = val; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
@@ -1002,6 +1004,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (m < 3 * n) { g->local_tiles = 16; g->local_max = 0xffffffffu; g->wl_local_tiles = 4; }
     else if (m >= 6 * n) g->local_tiles = 0;   // dense / skewed (rmat): measured no gain
     if (const char *lt = getenv("FALCON_WL_LOCAL")) g->wl_local_tiles = (uint32_t)atoi(lt);
+    if (const char *dc = getenv("FALCON_DELTA_CAP")) g->delta_cap = (uint32_t)atoi(dc);
     if (const char *lm = getenv("FALCON_WL_LOCAL_MAX")) g->wl_local_max = (uint32_t)atoll(lm);
     if (const char *lt = getenv("FALCON_LOCAL")) g->local_tiles = (uint32_t)atoi(lt);
     if (const char *lm = getenv("FALCON_LOCAL_MAX")) g->local_max = (uint32_t)atoll(lm);
@@ -1083,7 +1086,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->chunk = p->chunk; v->chunkb = p->chunkb; v->chunks = p->chunks;
     v->nblk = p->nblk; v->bsz = p->bsz; v->blk_bytes = p->blk_bytes;
     v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
-    v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max;
+    v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
     v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div;
     v->nwords = p->nwords; v->num_sms = p->num_sms;

@@ -63,7 +63,7 @@ struct Ctrl {
     uint32_t delta0;      // DELTA: initial bucket width (adaptive mode never goes below it)
     uint32_t delta_adapt; // DELTA: adapt the bucket width per bucket (auto Δ)
     uint32_t bk_rounds;   // DELTA: near rounds of the current bucket
-    uint32_t pad2_;
+    uint32_t delta_cap;   // DELTA: adaptive growth cap, in multiples of delta0
     unsigned long long bk_items;   // DELTA: items relaxed in the current bucket's near rounds
     uint32_t mode;        // DELTA: MODE_NEAR (relax the near queue) / MODE_SCAN (refill from far)
     uint32_t bar_arrive;  // persistent kernel: CTAs arrived at the grid barrier
@@ -107,6 +107,7 @@ struct Args {
     int32_t *const *peer_val;
     uint32_t *const *peer_bm;
     uint32_t delta_adapt;      // DELTA: adapt the bucket width per bucket (auto Δ)
+    uint32_t delta_cap;        // ... up to delta_cap x the initial width (0: 128)
     uint32_t local_tiles;      // SSSP DELTA sparse rounds: local continuation tiles per warp (0 = off)
     uint32_t local_max;        // ... in rounds of at most local_max items
     uint32_t wl_local_tiles;   // the same for SSSP WORKLIST sparse rounds
@@ -287,6 +288,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->pull = 0; c->found = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
         c->delta0 = delta; c->delta_adapt = a.delta_adapt; c->bk_rounds = 0; c->bk_items = 0;
+        c->delta_cap = a.delta_cap ? a.delta_cap : 128u;
         c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
@@ -1153,9 +1155,11 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
                 // of thresholds reaches the same fixpoint (T always moves past
                 // the smallest parked distance).
                 const unsigned long long avg = c->bk_items / (c->bk_rounds ? c->bk_rounds : 1u);
-                // (growth capped at 128 x the initial width: on a road grid the
-                // rounds stay small whatever Δ, and a larger Δ only adds work)
-                if (avg < (128ull << 10) && c->delta < 128u * c->delta0 && c->delta < (1u << 26)) c->delta *= 2u;
+                // (growth capped at delta_cap x the initial width: on a road grid
+                // the rounds stay small whatever Δ, and a larger Δ only adds work)
+                if (avg < (128ull << 10) && (uint64_t)c->delta < (uint64_t)c->delta_cap * c->delta0 &&
+                    c->delta < (1u << 26))
+                    c->delta *= 2u;
                 else if (avg > (2ull << 20) && c->delta / 2u >= c->delta0) c->delta /= 2u;
             }
             c->bk_items = 0;
