@@ -1,7 +1,4 @@
-# grid-24M DELTA / BFS WORKLIST per-round trace with and without local continuation (host-driven profiling mode)
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/trace.log 2>&1
-for L in 0 16; do
-  echo "== FALCON_LOCAL=$L (BFS unit-weight Δ-stepping needs local on)" >> gpurun_out/trace.log
-  FALCON_LOCAL=$L FALCON_TRACE=1 timeout 600 python tools/run_one.py --config grid-24M --algo sssp,bfs --style delta,worklist --reps 1 --profile > gpurun_out/trace_$L.out 2> gpurun_out/trace_$L.err
-  grep "rep0" gpurun_out/trace_$L.out >> gpurun_out/trace.log
-done
+# BFS VERTEX: bottom-up round inside the expansion kernel (one launch per round) -- parity + timing
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/pullmerge.log 2>&1
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_concurrent_gpu.py -x -q -k "bfs or small or layouts or golden or run_many" 2>&1 | tail -2 >> gpurun_out/pullmerge.log
+timeout 900 python tools/survey.py --configs rand-25M,rmat-10M,grid-24M --algos bfs --styles vertex --reps 5 2>&1 | grep -v "^==" >> gpurun_out/pullmerge.log
