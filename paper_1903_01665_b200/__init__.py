@@ -151,6 +151,24 @@ def _check_dtype(x, kind: str, name: str):
         raise TypeError(f"{name} must be {ok[0]}, got {s}")
 
 
+def _numel(x):
+    if hasattr(x, "numel"):
+        return int(x.numel())
+    if hasattr(x, "size") and not callable(x.size):
+        return int(x.size)
+    return None
+
+
+def _check_len(x, need: int, name: str, exact: bool = False):
+    """The C ABI reads / writes `need` elements through the pointer: a shorter
+    buffer would be overrun, so refuse it here."""
+    k = _numel(x)
+    if k is None:
+        return
+    if k < need or (exact and k != need):
+        raise ValueError(f"{name} has {k} elements, needs {'exactly ' if exact else 'at least '}{need}")
+
+
 class Graph:
     """Owning handle of a falcon_graph_t (freed by graph_free or on GC)."""
 
@@ -158,6 +176,7 @@ class Graph:
         self.handle = handle
         self.n = n
         self.m = m
+        self.out_len = n   # elements an output buffer must hold
 
     def __del__(self):
         try:
@@ -233,8 +252,11 @@ def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, strea
     """graph_load_csr(n, m, row_off u32[n+1], col u32[m], w i32[m] | None, ...)."""
     lib = load()
     _check_dtype(row_off, "u32", "row_off"); _check_dtype(col, "u32", "col")
+    _check_len(row_off, n + 1, "row_off")
+    _check_len(col, m, "col")
     if w is not None:
         _check_dtype(w, "i32", "w")
+        _check_len(w, m, "w")
     if stream is not None and hasattr(stream, "cuda_stream"):
         stream = stream.cuda_stream
     opts = _LoadOpts(device, ctypes.c_void_p(stream) if stream else None, flags,
@@ -273,6 +295,7 @@ def falcon_run_many(jobs) -> list:
     js = (_Job * k)(*[_Job(ALGOS[j[1]], _style(j[2]), int(j[3])) for j in jobs])
     for j in jobs:
         _check_dtype(j[4], "i32", "out")
+        _check_len(j[4], j[0].out_len, "out")
     outs = (ctypes.c_void_p * k)(*[_ptr(j[4]) for j in jobs])
     stats = (FalconStats * k)()
     _check(load().falcon_run_many(k, hs, js, outs, stats))
@@ -288,6 +311,7 @@ def graph_info(g: Graph):
 def falcon_sssp(g: Graph, source: int, style, dist_out) -> FalconStats:
     st = FalconStats()
     _check_dtype(dist_out, "i32", "dist_out")
+    _check_len(dist_out, g.out_len, "dist_out")
     _check(load().falcon_sssp(g.handle, source, _style(style), _ptr(dist_out), ctypes.byref(st)))
     return st
 
@@ -295,6 +319,7 @@ def falcon_sssp(g: Graph, source: int, style, dist_out) -> FalconStats:
 def falcon_bfs(g: Graph, source: int, style, level_out) -> FalconStats:
     st = FalconStats()
     _check_dtype(level_out, "i32", "level_out")
+    _check_len(level_out, g.out_len, "level_out")
     _check(load().falcon_bfs(g.handle, source, _style(style), _ptr(level_out), ctypes.byref(st)))
     return st
 
@@ -302,6 +327,7 @@ def falcon_bfs(g: Graph, source: int, style, level_out) -> FalconStats:
 def falcon_cc(g: Graph, style, label_out) -> FalconStats:
     st = FalconStats()
     _check_dtype(label_out, "i32", "label_out")
+    _check_len(label_out, g.out_len, "label_out")
     _check(load().falcon_cc(g.handle, _style(style), _ptr(label_out), ctypes.byref(st)))
     return st
 
@@ -326,6 +352,7 @@ def falcon_mst(g: Graph, style, label_out=None):
     st = FalconStats()
     if label_out is not None:
         _check_dtype(label_out, "i32", "label_out")
+        _check_len(label_out, g.out_len, "label_out")
     tot, ne = ctypes.c_int64(), ctypes.c_int64()
     _check(load().falcon_mst(g.handle, _style(style), ctypes.byref(tot), ctypes.byref(ne), _ptr(label_out),
                              ctypes.byref(st)))

@@ -455,17 +455,33 @@ falcon_status_t build_graph(falcon_graph *g, int algo, int style) {
 }
 
 falcon_status_t ensure_src(falcon_graph *g) {
-    if (g->src || g->m == 0) {
-        if (!g->src) CU(dmalloc(&g->src, 4));
+    if (g->src) return FALCON_OK;
+    if (g->m == 0) {
+        CU(dmalloc(&g->src, 4));
         return FALCON_OK;
     }
-    CU(dmalloc(&g->src, (size_t)g->m));
-    CU(dmalloc(&g->chunk, (size_t)((g->m + ECH_BFS - 1) / ECH_BFS)));
-    CU(dmalloc(&g->chunks, (size_t)((g->m + ECH_SSSP - 1) / ECH_SSSP)));
-    k_build_src<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->n, (uint32_t)g->m, g->row_off, g->src);
-    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH_BFS, g->src, g->chunk);
-    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH_SSSP, g->src, g->chunks);
-    CU(cudaGetLastError());
+    // built into locals and published only once complete: a failed build
+    // leaves the graph without the layout (the next call retries), never
+    // with a half-built one (falcon.h: the graph stays valid after an error)
+    uint32_t *src = nullptr;
+    uint2 *chunk = nullptr, *chunks = nullptr;
+    auto undo = [&] { dfree(src); dfree(chunk); dfree(chunks); };
+    if (dmalloc(&src, (size_t)g->m) != cudaSuccess ||
+        dmalloc(&chunk, (size_t)((g->m + ECH_BFS - 1) / ECH_BFS)) != cudaSuccess ||
+        dmalloc(&chunks, (size_t)((g->m + ECH_SSSP - 1) / ECH_SSSP)) != cudaSuccess) {
+        undo();
+        return fail(FALCON_ERR_NO_MEMORY, "COO sources: device allocation failed");
+    }
+    k_build_src<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->n, (uint32_t)g->m, g->row_off, src);
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH_BFS, src, chunk);
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, g->stream>>>((uint32_t)g->m, ECH_SSSP, src, chunks);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) {
+        undo();
+        return fail(FALCON_ERR_CUDA, "COO sources: %s", cudaGetErrorString(e));
+    }
+    g->src = src; g->chunk = chunk; g->chunks = chunks;
     return FALCON_OK;
 }
 
@@ -492,38 +508,58 @@ falcon_status_t ensure_blocked(falcon_graph *g) {
     const uint64_t len = K * (n + 1);
     const uint32_t ntiles = (uint32_t)((len + 1023) / 1024);
     uint32_t *tiles = g->tiles;
-    CU(dmalloc(&g->rowb, len));
-    CU(dmalloc(&g->cwb, m));
-    CU(dmalloc(&g->srcb, m));
-    k_blk_count<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->col, bsz, (uint32_t)K, g->rowb);
-    k_scan_local<<<ntiles, 256, 0, s>>>(g->rowb, len, tiles);
+    // built into locals, published only once complete (see ensure_src)
+    uint32_t *rowb = nullptr, *srcb = nullptr, *perm_in = nullptr, *perm = nullptr;
+    uint2 *cwb = nullptr, *chunkb = nullptr;
+    uint8_t *keys = nullptr, *keys_out = nullptr;
+    void *tmp = nullptr;
+    auto undo = [&] {
+        cudaStreamSynchronize(s);
+        dfree(rowb); dfree(srcb); dfree(cwb); dfree(chunkb);
+        dfree(keys); dfree(keys_out); dfree(perm_in); dfree(perm); dfree(tmp);
+    };
+#define BLK_TRY(call)                                                                             \
+    do {                                                                                          \
+        cudaError_t _e = (call);                                                                  \
+        if (_e != cudaSuccess) {                                                                  \
+            undo();                                                                               \
+            return fail(_e == cudaErrorMemoryAllocation ? FALCON_ERR_NO_MEMORY : FALCON_ERR_CUDA, \
+                        "destination-blocked layout: %s", cudaGetErrorString(_e));                \
+        }                                                                                         \
+    } while (0)
+    BLK_TRY(dmalloc(&rowb, len));
+    BLK_TRY(dmalloc(&cwb, m));
+    BLK_TRY(dmalloc(&srcb, m));
+    BLK_TRY(dmalloc(&chunkb, (size_t)((m + ECH_SSSP - 1) / ECH_SSSP)));
+    k_blk_count<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)n, g->row_off, g->col, bsz, (uint32_t)K, rowb);
+    k_scan_local<<<ntiles, 256, 0, s>>>(rowb, len, tiles);
     k_scan_tiles<<<1, 256, 0, s>>>(tiles, ntiles);
-    k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(g->rowb, len, tiles);
+    k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(rowb, len, tiles);
     {   // arcs grouped by target block, CSR order kept inside each block: a
         // stable radix sort of the arc indices by block id, then a gather
-        uint8_t *keys = nullptr, *keys_out = nullptr;
-        uint32_t *perm_in = nullptr, *perm = nullptr;
-        void *tmp = nullptr;
         size_t tmp_bytes = 0;
         int end_bit = 1;
         while ((1ull << end_bit) < K) end_bit++;
-        CU(dmalloc(&keys, m));
-        CU(dmalloc(&keys_out, m));
-        CU(dmalloc(&perm_in, m));
-        CU(dmalloc(&perm, m));
+        BLK_TRY(dmalloc(&keys, m));
+        BLK_TRY(dmalloc(&keys_out, m));
+        BLK_TRY(dmalloc(&perm_in, m));
+        BLK_TRY(dmalloc(&perm, m));
         k_blk_keys<<<g->num_sms * 8, BLOCK, 0, s>>>(m, g->col, bsz, keys, perm_in);
-        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_out, perm_in, perm, (int64_t)m, 0, end_bit,
-                                           s));
-        CU(dev_alloc(&tmp, tmp_bytes));
-        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, perm_in, perm, (int64_t)m, 0, end_bit, s));
-        k_blk_gather<<<g->num_sms * 8, BLOCK, 0, s>>>(m, perm, g->cw, g->src, g->cwb, g->srcb);
-        CU(cudaStreamSynchronize(s));
+        BLK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_out, perm_in, perm, (int64_t)m, 0,
+                                                end_bit, s));
+        BLK_TRY(dev_alloc(&tmp, tmp_bytes));
+        BLK_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, perm_in, perm, (int64_t)m, 0, end_bit,
+                                                s));
+        k_blk_gather<<<g->num_sms * 8, BLOCK, 0, s>>>(m, perm, g->cw, g->src, cwb, srcb);
+        BLK_TRY(cudaStreamSynchronize(s));
         dfree(keys); dfree(keys_out); dfree(perm_in); dfree(perm); dfree(tmp);
+        keys = keys_out = nullptr; perm_in = perm = nullptr; tmp = nullptr;
     }
-    CU(dmalloc(&g->chunkb, (size_t)((m + ECH_SSSP - 1) / ECH_SSSP)));
-    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH_SSSP, g->srcb, g->chunkb);
-    CU(cudaGetLastError());
-    CU(cudaStreamSynchronize(s));
+    k_chunk_range<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)m, ECH_SSSP, srcb, chunkb);
+    BLK_TRY(cudaGetLastError());
+    BLK_TRY(cudaStreamSynchronize(s));
+#undef BLK_TRY
+    g->rowb = rowb; g->cwb = cwb; g->srcb = srcb; g->chunkb = chunkb;
     g->nblk = (uint32_t)K;
     g->bsz = bsz;
     return FALCON_OK;
@@ -537,32 +573,51 @@ falcon_status_t ensure_reverse(falcon_graph *g) {
     if (g->rin_off) return FALCON_OK;
     const uint64_t n = (uint64_t)g->n, m = (uint64_t)g->m;
     cudaStream_t s = g->stream;
-    CU(dmalloc(&g->rin_off, n + 1));
-    CU(dmalloc(&g->rin_col, m));
-    if (!m) CU(cudaMemsetAsync(g->rin_off, 0, (n + 1) * 4, s));
     if (m) {
         falcon_status_t st = ensure_src(g);
         if (st != FALCON_OK) return st;
+    }
+    // built into locals, published only once complete (see ensure_src)
+    uint32_t *rin_off = nullptr, *rin_col = nullptr, *keys_out = nullptr;
+    void *tmp = nullptr;
+    auto undo = [&] {
+        cudaStreamSynchronize(s);
+        dfree(rin_off); dfree(rin_col); dfree(keys_out); dfree(tmp);
+    };
+#define REV_TRY(call)                                                                             \
+    do {                                                                                          \
+        cudaError_t _e = (call);                                                                  \
+        if (_e != cudaSuccess) {                                                                  \
+            undo();                                                                               \
+            return fail(_e == cudaErrorMemoryAllocation ? FALCON_ERR_NO_MEMORY : FALCON_ERR_CUDA, \
+                        "reverse CSR: %s", cudaGetErrorString(_e));                               \
+        }                                                                                         \
+    } while (0)
+    REV_TRY(dmalloc(&rin_off, n + 1));
+    REV_TRY(dmalloc(&rin_col, m ? m : 1));
+    if (!m) REV_TRY(cudaMemsetAsync(rin_off, 0, (n + 1) * 4, s));
+    if (m) {
         int end_bit = 1;
         while (end_bit < 32 && (1ull << end_bit) < n) end_bit++;
-        uint32_t *keys_out = nullptr;
-        void *tmp = nullptr;
         size_t tmp_bytes = 0;
-        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, g->col, keys_out, g->src, g->rin_col, (int64_t)m, 0,
-                                           end_bit, s));
-        CU(dmalloc(&keys_out, m));
-        CU(dev_alloc(&tmp, tmp_bytes));
-        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, g->col, keys_out, g->src, g->rin_col, (int64_t)m, 0,
-                                           end_bit, s));
+        REV_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, g->col, keys_out, g->src, rin_col, (int64_t)m, 0,
+                                                end_bit, s));
+        REV_TRY(dmalloc(&keys_out, m));
+        REV_TRY(dev_alloc(&tmp, tmp_bytes));
+        REV_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, g->col, keys_out, g->src, rin_col, (int64_t)m, 0,
+                                                end_bit, s));
         // in-row offsets from the sorted targets (first position of every
         // target, vertices without in-arcs included) -- no atomics
-        k_rin_off<<<g->num_sms * 8, BLOCK, 0, s>>>(m, (uint32_t)n, keys_out, g->rin_off);
-        CU(cudaStreamSynchronize(s));
+        k_rin_off<<<g->num_sms * 8, BLOCK, 0, s>>>(m, (uint32_t)n, keys_out, rin_off);
+        REV_TRY(cudaStreamSynchronize(s));
         dfree(keys_out);
         dfree(tmp);
+        keys_out = nullptr; tmp = nullptr;
     }
-    CU(cudaGetLastError());
-    CU(cudaStreamSynchronize(s));
+    REV_TRY(cudaGetLastError());
+    REV_TRY(cudaStreamSynchronize(s));
+#undef REV_TRY
+    g->rin_off = rin_off; g->rin_col = rin_col;
     return FALCON_OK;
 }
 
@@ -648,8 +703,12 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
     }
     cudaStream_t s = g->stream;
     Args a = g->args();
-    // round cap (R11): n + 2 (Bellman-Ford); DELTA adds one refill round per bucket
-    const int64_t capn = style == DELTA ? 2 * g->n + 4 : g->n + 2;
+    // round cap (R11): n + 2 (Bellman-Ford).  DELTA: SPEC.md:448's 10 n -- its
+    // refill rounds are not bounded by one per bucket (a vertex parked in the
+    // far set and later improved into the current bucket keeps its far bit and
+    // comes back in a later refill), so 2 n + 4 was not a bound
+    // (tests/test_overflow_gpu.py::test_delta_round_cap_chain).
+    const int64_t capn = style == DELTA ? 10 * g->n + 16 : g->n + 2;
     const uint32_t cap = (uint32_t)(capn > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : capn);
     uint32_t delta = 1;
     if (style == DELTA && !unit) {
@@ -777,6 +836,23 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
     return FALCON_OK;
 }
 
+// Overflow (reading R3): candidates >= INF are dropped during the fixpoint;
+// afterwards this decides, independent of the schedule, whether a reachable
+// vertex was left at INF (k_overflow_check), exactly when the oracle reports
+// a finite shortest distance >= INF.  Runs only after such a candidate.
+falcon_status_t overflow_certificate(falcon_graph *g, const uint32_t *row_off, const uint32_t *col, const int32_t *val,
+                                     bool *bad) {
+    cudaStream_t s = g->stream;
+    int flag = 0;
+    CU(cudaMemsetAsync(g->d_flags, 0, sizeof(int), s));
+    k_overflow_check<<<g->num_sms * 8, BLOCK, 0, s>>>((uint32_t)g->n, row_off, col, val, g->d_flags);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&flag, g->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *bad = flag != 0;
+    return FALCON_OK;
+}
+
 falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats) {
     if (g->pend_algo < 0) return fail(FALCON_ERR_INVALID_ARG, "no call in flight on this graph");
     const int algo = g->pend_algo;
@@ -796,9 +872,14 @@ falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats) {
         stats->relax_ms = g->pend_relax_ms;
         stats->relax_launches = g->pend_relax_launches;
     }
-    if (c.status == ST_OVERFLOW) return fail(FALCON_ERR_OVERFLOW, "a finite distance would reach FALCON_INF");
     if (c.status == ST_NOT_CONVERGED)
         return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", g->pend_cap);
+    if (algo == SSSP && c.cand_ovf) {   // some candidate reached INF: is a reachable vertex left at INF? (R3)
+        bool bad = false;
+        falcon_status_t st = overflow_certificate(g, g->row_off, g->col, g->val, &bad);
+        if (st != FALCON_OK) return st;
+        if (bad) return fail(FALCON_ERR_OVERFLOW, "a finite shortest distance is >= FALCON_INF");
+    }
     g_last_error.clear();
     return FALCON_OK;
 }
@@ -903,7 +984,6 @@ void destroy(falcon_graph *g) {
         g->parent->nviews--;
         g->row_off = g->col = g->src = g->rowb = g->srcb = g->rin_off = g->rin_col = g->tiles = nullptr;
         g->w = nullptr; g->cw = g->cwb = g->chunk = g->chunkb = g->chunks = g->cw_unit = nullptr;
-        g->d_flags = nullptr;
     }
     for (auto &row : g->execs)
         for (auto &x : row)
@@ -1112,6 +1192,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     CU(dmalloc(&v->fr1, n + 1));
     CU(dmalloc(&v->ctrl, 1));
     CU(dmalloc(&v->cnt, 3 * (size_t)v->cnt_slots));
+    CU(dmalloc(&v->d_flags, 1));   // the view's own (overflow certificate)
     CU(host_ctrl_alloc(reinterpret_cast<void **>(&v->h_ctrl), sizeof(Ctrl)));
     v->l2_window = p->l2_window;
     v->apw = p->apw;

@@ -72,7 +72,7 @@ struct Ctrl {
     uint32_t noq;         // WORKLIST: this (dense) round marks the bitmap only -- no queue is built
     uint32_t prevnoq;     // WORKLIST: the previous round did: read this round's items from the bitmap
     uint32_t hooks;       // MST: components hooked this round
-    uint32_t pad_;
+    uint32_t cand_ovf;    // SSSP: some candidate d[u]+w reached INF (k_overflow_check decides, reading R3)
     unsigned long long wsum;       // MST: total weight of the forest edges chosen so far
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
@@ -245,7 +245,7 @@ __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long
         c[0] += t0; c[1] += t1; c[2] += t2;
         if (t2) atomicAdd(&a.ctrl->found, (uint32_t)(t2 < 0xffffffffull ? t2 : 0xffffffffull));   // density heuristics
         if (s_flags & 1) a.ctrl->changed = 1;
-        if (s_flags & 2) a.ctrl->status = ST_OVERFLOW;
+        if (s_flags & 2) a.ctrl->cand_ovf = 1;   // not an error by itself (R3): checked after the fixpoint
     }
 }
 
@@ -289,7 +289,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
         c->delta0 = delta; c->delta_adapt = a.delta_adapt; c->bk_rounds = 0; c->bk_items = 0;
         c->delta_cap = a.delta_cap ? a.delta_cap : 128u;
-        c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0;
+        c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0; c->cand_ovf = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
 }
@@ -869,7 +869,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
         }
         if (lane == 0 && pm != 0xffffffffu) atomicMin(&c->minpend, pm);
     }
-    if (acc.ovf) c->status = ST_OVERFLOW;
+    if (acc.ovf) c->cand_ovf = 1;
 }
 
 // One round per launch (VERTEX, and the queue styles when not persistent).
@@ -1314,6 +1314,27 @@ __global__ void k_validate(uint32_t n, uint32_t m, const uint32_t *row_off, cons
         if (w && w[e] < 0) f |= 4;
     }
     if (f) atomicOr(flags, f);
+}
+
+// Overflow certificate (reading R3, run only when some candidate d[u]+w
+// reached INF during the fixpoint).  A candidate >= INF is never applied, so
+// every vertex whose least fixpoint distance is < INF still gets it exactly
+// (all prefixes of its shortest path stay below INF); a vertex reachable only
+// by paths of length >= INF stays at INF.  The oracle's overflow condition
+// (a finite shortest distance >= INF) is therefore equivalent to: some arc
+// u -> v has final val[u] < INF and final val[v] == INF -- schedule-free.
+// Rows may be a part's (empty outside its owned range); val is the full array.
+__global__ void k_overflow_check(uint32_t n, const uint32_t *row_off, const uint32_t *col, const int32_t *val,
+                                 int *flag) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    bool bad = false;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n && !bad; u += stride) {
+        if (val[u] == INF) continue;
+        const uint32_t e1 = row_off[u + 1];
+        for (uint32_t e = row_off[u]; e < e1; e++)
+            if (val[col[e]] == INF) { bad = true; break; }
+    }
+    if (bad) atomicOr(flag, 1);
 }
 
 __global__ void k_interleave(uint64_t m, const uint32_t *col, const int32_t *w, uint2 *cw) {

@@ -573,7 +573,9 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         if (st != FALCON_OK) return st;
         for (size_t i = 0; i < g->parts.size(); i++) {
             falcon_graph *p = g->parts[i];
-            args[i].lo = (uint32_t)p->lo; args[i].hi = (uint32_t)p->hi; args[i].nparts = (uint32_t)P;
+            // every part of the communicator (an NCCL rank holds only its own part)
+            args[i].lo = (uint32_t)p->lo; args[i].hi = (uint32_t)p->hi;
+            args[i].nparts = (uint32_t)(cm->simulated ? cm->simulated : cm->nranks);
             args[i].bounds = g->bounds_d; args[i].peer_val = g->d_peer_val; args[i].peer_bm = g->d_peer_bm;
         }
     }
@@ -707,6 +709,35 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
     for (size_t i = 0; i < g->parts.size(); i++)
         CU(cudaMemcpyAsync(&hc[i], g->parts[i]->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    bool overflow = false;
+    {   // overflow certificate (R3) over every part's rows against the gathered array
+        uint32_t any = 0;
+        for (auto &c : hc) any |= c.cand_ovf;
+        if (!cm->simulated) {   // the same decision on every rank
+            falcon_graph *me = g->parts[0];
+            CU(cudaMemcpyAsync(me->d_flags, &any, 4, cudaMemcpyHostToDevice, s));
+            NC(nc->AllReduce(me->d_flags, me->d_flags, 1, ncclUint32, ncclMax, cm->nccl, s));
+            CU(cudaMemcpyAsync(&any, me->d_flags, 4, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+        }
+        if (algo == SSSP && any) {
+            int flag = 0;
+            for (auto *p : g->parts) {
+                bool bad = false;
+                falcon_status_t st = overflow_certificate(p, p->row_off, p->col, dst, &bad);
+                if (st != FALCON_OK) return st;
+                flag |= bad ? 1 : 0;
+            }
+            if (!cm->simulated) {
+                falcon_graph *me = g->parts[0];
+                CU(cudaMemcpyAsync(me->d_flags, &flag, 4, cudaMemcpyHostToDevice, s));
+                NC(nc->AllReduce(me->d_flags, me->d_flags, 1, ncclInt32, ncclMax, cm->nccl, s));
+                CU(cudaMemcpyAsync(&flag, me->d_flags, 4, cudaMemcpyDeviceToHost, s));
+                CU(cudaStreamSynchronize(s));
+            }
+            overflow = flag != 0;
+        }
+    }
     dfree(staging);
     dfree(d_vals);
     dfree(d_ctrls);
@@ -725,10 +756,9 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         stats->ms = ms;
         stats->relax_ms = -1.0;
     }
-    for (auto &c : hc) {
-        if (c.status == ST_OVERFLOW) return fail(FALCON_ERR_OVERFLOW, "a finite distance would reach FALCON_INF");
+    for (auto &c : hc)
         if (c.status == ST_NOT_CONVERGED) return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", cap);
-    }
+    if (overflow) return fail(FALCON_ERR_OVERFLOW, "a finite shortest distance is >= FALCON_INF");
     g_last_error.clear();
     return FALCON_OK;
 }

@@ -69,3 +69,24 @@ def test_product_package_has_no_oracle_or_fallback():
             assert "import oracle" not in txt and "from oracle" not in txt, f
             assert "liboracle" not in txt, f
             assert "scipy" not in txt, f
+
+
+def test_binding_refuses_short_buffers(lib_path):
+    """ADVICE r1: the C ABI copies n values out and reads n+1 / m values in;
+    the binding checks lengths before calling into C."""
+    import numpy as np
+
+    import paper_1903_01665_b200 as fb
+    fb.load()
+    ro = np.array([0, 2, 3, 3], np.uint32)
+    with pytest.raises(ValueError, match="col"):
+        fb.graph_load_csr(3, 3, ro, np.array([1, 2], np.uint32), None)
+    with pytest.raises(ValueError, match="w"):
+        fb.graph_load_csr(3, 3, ro, np.array([1, 2, 0], np.uint32), np.array([1], np.int32))
+    with pytest.raises(ValueError, match="row_off"):
+        fb.graph_load_csr(3, 3, ro[:3], np.array([1, 2, 0], np.uint32), None)
+    g = fb.Graph(None, 5, 0)   # a handle-less graph: the length check comes first
+    for f in (lambda o: fb.falcon_sssp(g, 0, "vertex", o), lambda o: fb.falcon_bfs(g, 0, "vertex", o),
+              lambda o: fb.falcon_cc(g, "vertex", o)):
+        with pytest.raises(ValueError, match="elements"):
+            f(np.empty(4, np.int32))
