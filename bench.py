@@ -34,7 +34,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALGOS = ("sssp", "bfs", "cc")
-STYLES = ("vertex", "edge", "worklist")
+STYLES = ("vertex", "edge", "worklist", "delta")   # DELTA (Δ-stepping) is SSSP-only
+CLASS_CONFIGS = ("rand-25M", "rmat-10M")   # graph classes of the north_star's >= 50 % HBM target (random / RMAT)
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 
 
@@ -49,6 +50,7 @@ def parse():
     ap.add_argument("--impl", default="falcon", choices=["falcon", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-classes", action="store_true", help="skip the per-class best-style roofline (rmat-10M)")
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--mode", default="replica", choices=["replica", "sections", "partition"],
                     help="N>1: replica = one independent graph per GPU (weak scaling); sections = the same "
@@ -114,6 +116,63 @@ def l2_ops(algo, style, st):
     return E + U * 2 * pk["red_or_bitmap_cost_in_gathers"]
 
 
+def one_pass_bytes(algo, G) -> int:
+    """Work-efficient lower bound (each arc once): SSSP 12m+8n, BFS/CC 8m+8n."""
+    return (12 if algo == "sssp" else 8) * G.m + 8 * G.n
+
+
+def relax_roofline(cfg, algo, style, st, G, hbm, hbm_src, traffic, traffic_src):
+    """Roofline of one call's relax kernels: algorithmic bytes (SURVEY §8(d)
+    units, algorithmic_bytes) over the summed relax-kernel time measured
+    with CUDA events on the library stream (profiling mode); traffic = ncu
+    DRAM bytes per relax launch of the same (class, algo, style) call."""
+    b = algorithmic_bytes(algo, style, st, G.n, G.m)
+    achieved = b / (st["relax_ms"] * 1e-3) / 1e9
+    launches = max(1, st["relax_launches"])
+    t = traffic.get(f"{cfg}:{algo}/{style}")
+    r = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+         "traffic": t["dram_bytes"] / max(1, t["relax_launches"]) if t else None,
+         "kernel": f"relax {algo}/{style}", "config": cfg, "peak_source": hbm_src,
+         "relax_ms": st["relax_ms"], "relax_launches": st["relax_launches"], "algorithmic_bytes": b,
+         "algorithmic_bytes_per_launch": b / launches}
+    if t:
+        r["dram_over_algorithmic"] = t["dram_over_alg"]
+        r["lts_throughput_pct"] = t["lts_throughput_pct_time_weighted"]
+        r["traffic_source"] = traffic_src
+    try:   # secondary ceiling: random L2 operations (DESIGN.md §6)
+        pk = json.load(open(os.path.join(ROOT, "profiles", "l2_peaks.json")))
+        ops = l2_ops(algo, style, st)
+        ach = ops / (st["relax_ms"] * 1e-3) / 1e9
+        r["l2_ops"] = {"achieved": ach, "peak": pk["gather_gops_window_le_64MB"], "unit": "G gather-slots/s",
+                       "frac": ach / pk["gather_gops_window_le_64MB"], "ops": ops,
+                       "peak_source": "profiles/l2_peaks.json (tools/l2probe3.cu)"}
+    except (OSError, KeyError, ValueError):
+        pass
+    return r
+
+
+def best_block(cfg, G, g, med, prof, fb, hbm, hbm_src, traffic, traffic_src, algos, out):
+    """Per algorithm: the fastest style by median ms and the roofline of its
+    relax kernels (one profiled call unless the step's profile has it)."""
+    blk = {}
+    for a in algos:
+        cands = {s: ms for (aa, s), ms in med.items() if aa == a}
+        if not cands:
+            continue
+        s = min(cands, key=cands.get)
+        st = prof[(a, s)][0] if prof and (a, s) in prof else None
+        if st is None:
+            fb.falcon_set_profiling(g, True)
+            st = fb.run(g, a, s, out, G.source).as_dict()
+            fb.falcon_set_profiling(g, False)
+        r = relax_roofline(cfg, a, s, st, G, hbm, hbm_src, traffic, traffic_src)
+        r.update({"style": s, "ms": cands[s], "ms_by_style": {k: round(v, 4) for k, v in cands.items()},
+                  "one_pass_eff": one_pass_bytes(a, G) / (cands[s] * 1e-3) / 1e9 / hbm,
+                  "edges_relaxed_over_m": st["edges_relaxed"] / max(1, G.m), "iterations": st["iterations"]})
+        blk[a] = r
+    return blk
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -171,26 +230,41 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def ncu_traffic(kernel_key: str):
-    """dram read+write bytes per launch for the dominant kernel, from the
-    committed ncu --set full summary (profiles/ncu_traffic.json), else None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(p):
-        return None
-    d = json.load(open(p))
-    v = d.get(kernel_key)
-    return None if v is None else float(v.get("dram_bytes_per_launch"))
+def traffic_table():
+    """ncu DRAM bytes of the relax kernels per (class, algo, style) call
+    (tools/traffic.py, committed under profiles/), newest round first."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            return json.load(open(p))["calls"], os.path.relpath(p, ROOT)
+        except (OSError, KeyError, ValueError):
+            continue
+    return {}, None
 
 
 # ------------------------------------------------------------------ CPU oracle legs
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_pass(G, algos):
-    """One oracle pass (each algorithm once, concurrently in threads: ctypes
-    releases the GIL).  Returns (m_counted total, wall seconds, threads)."""
+    """One oracle pass: each algorithm once, single-threaded, the three
+    concurrently in host threads (ctypes releases the GIL).  Each oracle's own
+    wall time is taken on its thread with the monotonic (steady) clock.
+    Returns (m_counted total, pass wall seconds, threads, per-oracle seconds)."""
     import oracle
-    res = {}
+    res, per = {}, {}
 
     def one(a):
+        t0 = time.perf_counter()   # CLOCK_MONOTONIC
         res[a] = oracle.run(a, G)
+        per[a] = time.perf_counter() - t0
 
     ths = [threading.Thread(target=one, args=(a,)) for a in algos]
     t0 = time.perf_counter()
@@ -199,7 +273,7 @@ def oracle_pass(G, algos):
     for t in ths:
         t.join()
     dt = time.perf_counter() - t0
-    return sum(m_counted(G, a, res[a]) for a in algos), dt, len(algos)
+    return sum(m_counted(G, a, res[a]) for a in algos), dt, len(algos), per
 
 
 def reference_arm(args, rank, world):
@@ -213,9 +287,9 @@ def reference_arm(args, rank, world):
     for _ in range(args.warmup):          # warm-up on the tiny config (page-in, caches)
         oracle_pass(tiny, algos)
     steps = max(1, min(args.steps, args.ref_max_steps))
-    tot_m, tot_t, cores = 0, 0.0, len(algos)
+    tot_m, tot_t, cores, per = 0, 0.0, len(algos), {}
     for _ in range(steps):
-        mc, dt, cores = oracle_pass(G, algos)
+        mc, dt, cores, per = oracle_pass(G, algos)
         tot_m += mc
         tot_t += dt
     value = tot_m / tot_t / 1e9
@@ -226,7 +300,8 @@ def reference_arm(args, rank, world):
             "ms_per_step": 1e3 * tot_t / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
             "config": {"workload": args.config, "n": G.n, "m": G.m, "algos": algos, "styles": ["oracle"]},
-            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample,
+                             "per_oracle_s": per, "cpu_model": cpu_model(), "host_threads": os.cpu_count()},
             "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line, args)
 
@@ -340,6 +415,7 @@ def main():
     # ---- roofline of the dominant kernel: one profiled step (host-driven loop,
     # CUDA events around every relax launch on the library stream)
     hbm, hbm_src = peaks()
+    traffic, traffic_src = traffic_table()
     prof = {}
     roofline = None
     if not partition and runs:
@@ -348,24 +424,8 @@ def main():
         fb.falcon_set_profiling(g, False)
         shares = {k: v[0]["relax_ms"] for k, v in prof.items()}
         dom = max(shares, key=shares.get)
-        dst = prof[dom][0]
-        bytes_dom = algorithmic_bytes(dom[0], dom[1], dst, G.n, G.m)
-        achieved = bytes_dom / (dst["relax_ms"] * 1e-3) / 1e9
-        key = f"{dom[0]}/{dom[1]}"
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": ncu_traffic(key), "kernel": f"relax {key}", "peak_source": hbm_src,
-                    "relax_ms": dst["relax_ms"], "relax_launches": dst["relax_launches"],
-                    "algorithmic_bytes": bytes_dom, "share_of_step": dst["relax_ms"] / ms_step}
-        # secondary ceiling: random L2 operations (the path's real bound)
-        try:
-            pk = json.load(open(os.path.join(ROOT, "profiles", "l2_peaks.json")))
-            ops = l2_ops(dom[0], dom[1], dst)
-            ach = ops / (dst["relax_ms"] * 1e-3) / 1e9
-            roofline["l2_ops"] = {"achieved": ach, "peak": pk["gather_gops_window_le_64MB"], "unit": "G gather-slots/s",
-                                  "frac": ach / pk["gather_gops_window_le_64MB"], "ops": ops,
-                                  "peak_source": "profiles/l2_peaks.json (tools/l2probe3.cu)"}
-        except (OSError, KeyError, ValueError):
-            pass
+        roofline = relax_roofline(args.config, dom[0], dom[1], prof[dom][0], G, hbm, hbm_src, traffic, traffic_src)
+        roofline["share_of_step"] = prof[dom][0]["relax_ms"] / ms_step
     elif partition:   # partitioned: the whole superstep loop (relax + exchange) of the slowest algorithm
         worst = max(per_run, key=lambda k: statistics.median(x["ms"] for x in per_run[k]))
         x = per_run[worst][-1]
@@ -387,7 +447,30 @@ def main():
                                  "edges_relaxed": x["edges_relaxed"], "updates": x["updates"],
                                  "relax_ms": p["relax_ms"], "alg_GBps_relax": bts / (p["relax_ms"] * 1e-3) / 1e9
                                  if p["relax_ms"] and p["relax_ms"] > 0 else None,
-                                 "one_pass_eff": ((12 if a == "sssp" else 8) * G.m + 8 * G.n) / (ms * 1e-3) / 1e9 / hbm}
+                                 "one_pass_eff": one_pass_bytes(a, G) / (ms * 1e-3) / 1e9 / hbm}
+
+    # ---- best processing style per graph class (north_star: >= 50 % of HBM
+    # for the best style on random / RMAT graphs at 1 GPU): the fastest style
+    # of each algorithm by median ms, and the roofline of ITS relax kernels
+    best = None
+    if not partition and world == 1 and not args.no_classes:
+        best = {}
+        for cfg in CLASS_CONFIGS:
+            if cfg == args.config:
+                med = {k: statistics.median(x["ms"] for x in v) for k, v in per_run.items()}
+                best[cfg] = best_block(cfg, G, g, med, prof, fb, hbm, hbm_src, traffic, traffic_src, algos, out)
+            else:
+                Gc = gg.config(cfg)
+                gc = fb.graph_load_csr(Gc.n, Gc.m, Gc.row_off, Gc.col, Gc.w, device=local, stream=stream,
+                                       flags=fb.LOAD_BUILD_COO)
+                oc = torch.empty(Gc.n, dtype=torch.int32, device="cuda")
+                med = {}
+                for a, s_ in all_runs:
+                    fb.run(gc, a, s_, oc, Gc.source)   # warm-up (lazy layouts, CUDA graphs)
+                    med[(a, s_)] = statistics.median(fb.run(gc, a, s_, oc, Gc.source).ms for _ in range(5))
+                best[cfg] = best_block(cfg, Gc, gc, med, None, fb, hbm, hbm_src, traffic, traffic_src, algos, oc)
+                fb.graph_free(gc)
+                del Gc
 
     # ---- e2e through the C ABI with HOST buffers (H2D + D2H inside the timed region)
     e2e = None
@@ -424,10 +507,12 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tot, dt, cores = oracle_pass(G, algos)
+        tot, dt, cores, per = oracle_pass(G, algos)
         cpu = {"value": tot / dt / 1e9, "unit": "GTEPS", "cores": cores, "kind": "oracle",
                "sample": f"one oracle pass ({'+'.join(algos)}, one algorithm per host thread, single-threaded "
-                         f"each) over {args.config}: {dt:.1f} s wall; host has {os.cpu_count()} cores"}
+                         f"each) over {args.config}: {dt:.1f} s wall",
+               "per_oracle_s": {a: round(v, 3) for a, v in per.items()}, "cpu_model": cpu_model(),
+               "host_threads": os.cpu_count()}
 
     if rank == 0:
         line = {"metric": "SSSP/BFS/CC GTEPS (aggregate over runs per step)", "value": value, "unit": "GTEPS",
@@ -443,7 +528,7 @@ def main():
                                  else ("replicas" if world > 1 else "single")),
                            "l2": "inputs larger than L2 (CSR+COO %.2f GB vs 126 MB L2); each run re-initialises "
                                  "its value array" % ((4 * (G.n + 1) + 12 * G.m) / 1e9)},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "best_style": best, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "per_run": breakdown}
         emit(line, args)
     fb.graph_free(g)

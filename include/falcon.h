@@ -64,8 +64,10 @@ typedef enum {
     FALCON_ERR_OUT_OF_RANGE = 2,  /* row_off not 0..m nondecreasing, col >= n, w < 0, src >= n */
     FALCON_ERR_NO_MEMORY = 3,     /* device allocation failed                                  */
     FALCON_ERR_CUDA = 4,          /* any other CUDA runtime error (graph may be unusable)      */
-    FALCON_ERR_OVERFLOW = 5,      /* a finite distance would reach FALCON_INF                  */
-    FALCON_ERR_NOT_CONVERGED = 6, /* iteration cap (n + 2 rounds; DELTA 2n + 4) exceeded        */
+    FALCON_ERR_OVERFLOW = 5,      /* SSSP: some vertex's shortest distance is finite but
+                                     >= FALCON_INF (decided on the final distances, so the status
+                                     never depends on the relaxation schedule; R3)    */
+    FALCON_ERR_NOT_CONVERGED = 6, /* iteration cap (n + 2 rounds; DELTA 10 n)      */
     FALCON_ERR_COMM = 7,          /* reserved: multi-GPU communication failure                 */
     FALCON_ERR_UNSUPPORTED = 8    /* option not supported by this build                        */
 } falcon_status_t;
