@@ -2,20 +2,25 @@
 """Benchmark of the fixpoint min-relaxation hot path (SSSP / BFS / CC).
 
 One STEP = one pass of the whole hot path over the workload graph: every
-algorithm (SSSP, BFS, CC) in every processing style (VERTEX, EDGE, WORKLIST)
-through the C ABI, i.e. 9 library calls, each doing init -> device-side
-fixpoint loop -> output (graph residency a1 is
-outside the timed region except in the e2e number).
+algorithm (SSSP, BFS, CC) in every processing style (VERTEX, EDGE, WORKLIST;
+SSSP also DELTA) through the C ABI, i.e. 10 library calls, each doing init ->
+device-side fixpoint loop -> output (graph
+residency a1 is outside the timed region except in the e2e number).
 
 Metric (BASELINE.json): GTEPS = sum over the step's runs of m_counted / time,
 m_counted = arcs whose source is reached (SSSP/BFS; Graph500-style, DESIGN.md
-R13) or m (CC).  value is the whole-job aggregate over all ranks.
+R13) or m (CC).  value is the whole-job aggregate over all ranks.  The line
+also carries the roofline of the step's dominant relax kernel and, per graph
+class (rand-25M, rmat-10M), the roofline of the best (fastest) style of each
+algorithm (`best_style`).
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config rand-25M]
         python bench.py --impl reference ...   (the CPU oracle, timed on host cores)
-Multi-GPU (N>1, torchrun): "parallel sections" replica mode of PAPER.md:1587-1597
--- every rank runs the step on its own seeded instance (weak scaling); there is
-no data-path collective.
+Multi-GPU (N>1, torchrun): by default the graph is 1-D vertex-partitioned
+over the N GPUs (each rank loads only its row slice, boundary
+values travel over NVLink; strong scaling); --mode replica / sections run
+the paper's own multi-GPU shapes (independent graphs / "parallel sections",
+PAPER.md:1587-1597) instead.  --simulate P runs P partitions on one GPU.
 """
 from __future__ import annotations
 
@@ -52,12 +57,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-classes", action="store_true", help="skip the per-class best-style roofline (rmat-10M)")
     ap.add_argument("--ref-max-steps", type=int, default=3)
-    ap.add_argument("--mode", default="replica", choices=["replica", "sections", "partition"],
-                    help="N>1: replica = one independent graph per GPU (weak scaling); sections = the same "
-                         "graph on every GPU, the step's (algo, style) runs dealt round-robin to the GPUs "
-                         "(PAPER.md:1587-1597 'parallel sections', SURVEY §8(f) row 2; strong scaling, "
-                         "time = max over GPUs); partition = one graph 1-D vertex-partitioned over the "
-                         "GPUs with NCCL exchange (SURVEY.md §8(e), strong scaling)")
+    ap.add_argument("--mode", default=None, choices=["replica", "sections", "partition"],
+                    help="N>1 (default: partition): partition = one graph 1-D vertex-partitioned over the GPUs, "
+                         "each rank loading only its row slice, boundary exchange over NVLink (SURVEY.md §8(e), "
+                         "strong scaling); replica = one independent graph per GPU (weak scaling); sections = "
+                         "the same graph on every GPU, the step's (algo, style) runs dealt round-robin to the "
+                         "GPUs (PAPER.md:1587-1597 'parallel sections', SURVEY §8(f) row 2; time = max over GPUs)")
     ap.add_argument("--simulate", type=int, default=0,
                     help="partition mode on ONE GPU with this many simulated parts (device-side exchange)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -341,6 +346,8 @@ def main():
     algos = [a for a in args.algos.split(",") if a]
     styles = [s for s in args.styles.split(",") if s]
 
+    if args.mode is None:
+        args.mode = "partition" if world > 1 else "single"
     partition = args.mode == "partition" or args.simulate > 0
     # Workload: the BASELINE.json config; replica r uses seed + r (weak scaling);
     # partition mode: the same graph on every rank (each keeps its rows).
@@ -363,9 +370,17 @@ def main():
                 dist.broadcast_object_list(obj, src=0)
             comm = fb.falcon_comm_init(world, rank, obj[0], local)
         styles = ["vertex"]   # the partitioned path runs the VERTEX round on every part
-    g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream,
-                          flags=0 if partition else fb.LOAD_BUILD_COO, comm=comm)
-    out = torch.empty(G.n, dtype=torch.int32, device="cuda")
+    if partition and not args.simulate:   # each rank passes only its own rows (FALCON_LOAD_SLICE)
+        bounds = fb.falcon_partition(G.row_off, world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        base, top = int(G.row_off[lo]), int(G.row_off[hi])
+        g = fb.graph_load_csr(hi - lo, top - base, (G.row_off[lo:hi + 1] - base).astype(np.uint32),
+                              G.col[base:top], G.w[base:top], device=local, stream=stream, flags=fb.LOAD_SLICE,
+                              comm=comm)
+    else:
+        g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream,
+                              flags=0 if partition else fb.LOAD_BUILD_COO, comm=comm)
+    out = torch.empty(g.out_len, dtype=torch.int32, device="cuda")
     all_runs = [(a, s) for a in algos for s in styles if s != "delta" or a == "sssp"]   # DELTA is SSSP-only
     runs = all_runs[rank::world] if sections else all_runs   # parallel sections: this GPU's share
 
@@ -378,11 +393,23 @@ def main():
                 collect.setdefault((a, s), []).append(st.as_dict())
         return launches
 
-    # m_counted per run (outputs are unique fixpoints: style-independent)
+    # m_counted per run (outputs are unique fixpoints: style-independent);
+    # a rank's output is its owned slice: count its rows, sum over ranks
     mc = {}
+    glo, ghi = fb.graph_owned_range(g) if comm is not None else (0, G.n)
     for a in algos:
         fb.run(g, a, styles[0], out, G.source)
-        mc[a] = m_counted(G, a, out.cpu().numpy())
+        o = out.cpu().numpy()
+        if len(o) == G.n:
+            mc[a] = m_counted(G, a, o)
+        else:
+            deg = np.diff(G.row_off[glo:ghi + 1].astype(np.int64))
+            c = int(G.row_off[ghi]) - int(G.row_off[glo]) if a == "cc" else int(deg[o != 2147483647].sum())
+            if dist:
+                t = torch.tensor([c], dtype=torch.int64, device="cuda" if args.dist_backend == "nccl" else "cpu")
+                dist.all_reduce(t)
+                c = int(t.item())
+            mc[a] = c
     units_per_step = sum(mc[a] for a, _ in (all_runs if sections else runs))   # sections: all GPUs' runs
 
     for _ in range(args.warmup):
@@ -437,6 +464,39 @@ def main():
                     "kernel": f"partitioned superstep loop {worst[0]} (relax + exchange, all parts)",
                     "peak_source": hbm_src + (" x ranks" if world > 1 else ""), "algorithmic_bytes": bytes_dom}
 
+    # ---- partitioned runs: exchange volume, supersteps, host round trips,
+    # and (rank 0, same run) the 1-GPU time of the same calls on the full graph
+    part = None
+    if partition:
+        names = {1: "dense", 2: "sparse", 3: "fused"}
+        info = {}
+        for a in algos:
+            st = fb.run(g, a, "vertex", out, G.source)
+            xb = fb.graph_exchange_bytes(g)
+            mode_, steps, checks = fb.graph_partition_info(g)
+            info[a] = {"ms": st.ms, "exchange": names.get(mode_, mode_), "exchange_bytes_this_rank": xb,
+                       "supersteps": steps, "host_round_trips": checks,
+                       "nvlink_frac_of_900GBps": (xb / (st.ms * 1e-3) / 900e9) if st.ms > 0 and not args.simulate
+                       else None}
+        t1 = None
+        if rank == 0:
+            g1 = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=local, stream=stream)
+            o1 = torch.empty(G.n, dtype=torch.int32, device="cuda")
+            t1 = {}
+            for a in algos:
+                fb.run(g1, a, "vertex", o1, G.source)
+                t1[a] = statistics.median(fb.run(g1, a, "vertex", o1, G.source).ms for _ in range(3))
+            fb.graph_free(g1)
+            del o1
+        if dist:
+            dist.barrier()
+        P_ = world if not args.simulate else args.simulate
+        tP = {a: statistics.median(x["ms"] for x in per_run[(a, "vertex")]) for a in algos if (a, "vertex") in per_run}
+        part = {"parts": P_, "per_algo": info, "t1_ms_same_run": t1, "tP_ms": tP,
+                "t1_over_P_tP": {a: t1[a] / (P_ * tP[a]) for a in tP} if t1 and not args.simulate else None,
+                "note": "t1 = the same calls (VERTEX style) on the full graph on rank 0's GPU in this run; "
+                        "exchange bytes: this rank's sends (fused: 8 B per remote improvement)"}
+
     breakdown = {}
     for (a, s), lst in per_run.items():
         ms = statistics.median(x["ms"] for x in lst)
@@ -475,13 +535,20 @@ def main():
     # ---- e2e through the C ABI with HOST buffers (H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
-        pin = lambda a: torch.from_numpy(a).pin_memory()
-        h_ro, h_col, h_w = pin(G.row_off), pin(G.col), pin(G.w)
-        h_out = torch.empty(G.n, dtype=torch.int32).pin_memory()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        sliced = partition and not args.simulate   # a rank copies only its own rows (FALCON_LOAD_SLICE)
+        if sliced:
+            h_ro = pin((G.row_off[lo:hi + 1] - base).astype(np.uint32))
+            h_col, h_w = pin(G.col[base:top]), pin(G.w[base:top])
+            e_n, e_m, e_flags = hi - lo, top - base, fb.LOAD_SLICE
+        else:
+            h_ro, h_col, h_w = pin(G.row_off), pin(G.col), pin(G.w)
+            e_n, e_m, e_flags = G.n, G.m, 0
+        h_out = torch.empty(g.out_len, dtype=torch.int32).pin_memory()
         e_steps = max(1, min(args.steps, 3))
 
         def e2e_step():
-            gh = fb.graph_load_csr(G.n, G.m, h_ro, h_col, h_w, device=local, stream=stream, comm=comm)
+            gh = fb.graph_load_csr(e_n, e_m, h_ro, h_col, h_w, device=local, stream=stream, comm=comm, flags=e_flags)
             for a, s in runs:
                 fb.run(gh, a, s, h_out, G.source)
             fb.graph_free(gh)
@@ -502,7 +569,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": replicas * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",
-               "h2d_bytes_per_step": 4 * (G.n + 1) + 8 * G.m, "d2h_bytes_per_step": 4 * G.n * len(all_runs),
+               "h2d_bytes_per_step": 4 * (e_n + 1) + 8 * e_m, "d2h_bytes_per_step": 4 * g.out_len * len(runs),
                "steps": e_steps, "ms_per_step": ems / e_steps}
 
     cpu = None
@@ -528,7 +595,7 @@ def main():
                                  else ("replicas" if world > 1 else "single")),
                            "l2": "inputs larger than L2 (CSR+COO %.2f GB vs 126 MB L2); each run re-initialises "
                                  "its value array" % ((4 * (G.n + 1) + 12 * G.m) / 1e9)},
-                "roofline": roofline, "best_style": best, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "best_style": best, "partition": part, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "per_run": breakdown}
         emit(line, args)
     fb.graph_free(g)

@@ -79,6 +79,20 @@ typedef struct falcon_comm falcon_comm_t;   /* opaque; multi-GPU communicator (N
 #define FALCON_LOAD_BUILD_COO 0x1u      /* build the COO src[] array now (else lazily on first EDGE call) */
 #define FALCON_LOAD_BUILD_REVERSE 0x2u  /* build the reverse (in-arc) CSR now (else lazily on the first BFS
                                            VERTEX / CC WORKLIST call) */
+/* Partitioned graphs (opts.comm != NULL) only -- per-GPU graph copies of the
+ * paper's multi-GPU runs (§3.4) without the full graph on
+ * every rank: */
+#define FALCON_LOAD_SLICE 0x4u   /* this rank passes ONLY its own rows: n = rows of the slice, m = their arcs,
+                                    row_off = the slice's offsets (row_off[0] == 0, row_off[n] == m), col =
+                                    GLOBAL target ids.  The ranks' slices, in rank order, are the graph: rank
+                                    r owns the vertices after those of ranks < r (all-gathered at load; the
+                                    global n is their total).  Needs a rank communicator (NCCL or loopback),
+                                    not a simulated one (UNSUPPORTED).  Validated on the device against the
+                                    global n -- no full-graph host copy. */
+#define FALCON_LOAD_GATHER 0x8u  /* every algorithm call writes the FULL n-length output on every rank (an
+                                    all-gather of the owned slices).  Default for rank communicators: each
+                                    rank receives only its owned slice [lo, hi) (graph_owned_range), an
+                                    int32[hi - lo] buffer.  Simulated graphs always return the full array. */
 
 typedef struct {
     int device;          /* CUDA device ordinal; -1 = current device                 */
@@ -114,14 +128,21 @@ FALCON_API falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *
                                const int32_t *w, const falcon_load_opts_t *opts, falcon_graph_t **out);
 
 /* ---- multi-GPU: 1-D vertex partition ----
- * Vertices are split into contiguous ranges of ~m/P arcs each; part q stores
- * the CSR rows of its range and exchanges boundary values once per round
- * (grouped ncclReduce(MIN) to the owners, ncclAllReduce(SUM) termination).
- * Every rank passes the FULL CSR to graph_load_csr (it keeps only its rows)
- * and calls the algorithms collectively, in the same order; every rank
- * receives the FULL n-length output.  Results equal the single-GPU ones.
- * BFS runs as unit-weight SSSP; CC hooks on a replicated label array.  The
- * processing style is ignored (every part runs the VERTEX round). */
+ * Vertices are split into contiguous ranges; part q stores the CSR rows of
+ * its range.  Either every rank passes the FULL CSR (ranges of ~m/P arcs are
+ * chosen by binary search on row_off; each rank keeps only its rows) or each
+ * rank passes only its own rows (FALCON_LOAD_SLICE).  All ranks then call the
+ * algorithms collectively, in the same order.  Per superstep the boundary
+ * values travel by the "exchange" option (falcon_set_option): by default the
+ * relax kernel itself writes every remote improvement into its owner's arrays
+ * over peer memory (NVLink via CUDA IPC) -- fused, no exchange step -- else a
+ * grouped ncclReduce(MIN) to the owners (dense) or (vertex, value) pairs
+ * (sparse); termination is an ncclAllReduce(SUM) of the round's `changed`
+ * flag, and the host checks for the fixpoint once every 4 supersteps.  Output:
+ * the owned slice per rank, or the full array with FALCON_LOAD_GATHER.
+ * Results equal the single-GPU ones.  BFS runs as unit-weight SSSP; CC hooks
+ * on a replicated label array (ncclAllReduce(MIN) per round).  The processing
+ * style is ignored (every part runs the VERTEX round). */
 
 /* Partition boundaries: bounds[q] .. bounds[q+1] is part q's vertex range,
  * chosen so each part owns ~m/nparts arcs (binary search on row_off).
@@ -133,8 +154,19 @@ FALCON_API falcon_status_t falcon_partition(int64_t n, const uint32_t *row_off, 
 FALCON_API falcon_status_t falcon_comm_unique_id(void *id128);
 
 /* One rank of an nranks-wide communicator on `device` (one process per GPU;
- * NCCL over NVLink / NVSwitch).  Errors: INVALID_ARG, COMM, CUDA. */
+ * NCCL over NVLink / NVSwitch), or of a loopback world when id128 comes from
+ * falcon_comm_loopback_id.  Errors: INVALID_ARG, COMM, CUDA. */
 FALCON_API falcon_status_t falcon_comm_init(int nranks, int rank, const void *id128, int device, falcon_comm_t **out);
+
+/* A 128-byte id for an in-process LOOPBACK communicator of nranks ranks: pass
+ * it to falcon_comm_init from nranks host threads of THIS process (any device,
+ * typically the same one).  The ranks then run exactly the code path of NCCL
+ * ranks -- slice loading, exchanges, termination, owned-slice output -- with
+ * every NCCL call served in-process (device copies, host barriers): how the
+ * per-rank multi-GPU path is tested on a one-GPU box (NCCL refuses two ranks
+ * on one device).  Free each rank's communicator with falcon_comm_free.
+ * Errors: INVALID_ARG (nranks not in [1, 64]), NO_MEMORY. */
+FALCON_API falcon_status_t falcon_comm_loopback_id(int nranks, void *id128);
 
 /* A simulated communicator: nparts partitions on the current device of ONE
  * process, exchanged by device kernels (same partition, relax, apply and
@@ -144,14 +176,25 @@ FALCON_API falcon_status_t falcon_comm_init_simulated(int nparts, falcon_comm_t 
 FALCON_API falcon_status_t falcon_comm_free(falcon_comm_t *comm);
 
 /* Vertex range [lo, hi) owned by this rank ([0, n) for a single-GPU or a
- * simulated graph). */
+ * simulated graph); the output of a rank's call is this slice unless the
+ * graph was loaded with FALCON_LOAD_GATHER. */
 FALCON_API falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi);
 
 /* Bytes the last call on a partitioned graph moved in its boundary exchanges
  * (dense reduce-scatter rounds: 4 bytes per exchanged vertex; sparse rounds:
- * 8 bytes per (vertex, value) pair; this rank's sends, or all parts when
- * simulated).  0 for a single-GPU graph. */
+ * 8 bytes per (vertex, value) pair; fused rounds: 8 bytes -- a RED.MIN and a
+ * bitmap RED.OR -- per remote improvement; CC: the 4n-byte label all-reduce
+ * per round; this rank's sends, or all parts when simulated).  0 for a
+ * single-GPU graph. */
 FALCON_API falcon_status_t graph_exchange_bytes(const falcon_graph_t *g, int64_t *bytes);
+
+/* The last call on a partitioned graph: *exchange_mode = the exchange its
+ * supersteps used (1 dense, 2 sparse, 3 fused), *supersteps = rounds run,
+ * *host_checks = host round trips of the fixpoint loop (one per 4 supersteps;
+ * the sparse exchange adds its per-superstep count syncs).  Any pointer may be
+ * NULL.  Errors: INVALID_ARG (NULL g), UNSUPPORTED (not partitioned). */
+FALCON_API falcon_status_t graph_partition_info(const falcon_graph_t *g, int32_t *exchange_mode, int64_t *supersteps,
+                                                int64_t *host_checks);
 
 /* Release the graph's device memory (to the library's device-memory cache,
  * which later loads reuse; a failed allocation releases the cache).  NULL is a
@@ -257,12 +300,22 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  * Changing an option drops the cached CUDA graphs (and, for block_bytes, the
  * blocked layout); they are rebuilt on the next call.
  *   "exchange"     partitioned graphs: boundary exchange per superstep, 0 = auto
- *                  (sparse pairs when smaller than the dense reduce-scatter),
- *                  1 = dense, 2 = sparse, 3 = fused (relax kernels write remote
- *                  targets into their owners' arrays over peer memory; NCCL
- *                  ranks map each other's arrays with CUDA IPC) (env FALCON_EXCHANGE)
+ *                  (fused between ranks that can map each other's memory,
+ *                  else dense; dense for simulated parts), 1 = dense
+ *                  (grouped ncclReduce(MIN) per owner), 2 = sparse ((vertex,
+ *                  value) pairs by ncclSend / ncclRecv; host-synchronised
+ *                  per superstep), 3 = fused (relax kernels RED.MIN / RED.OR
+ *                  remote targets into their owners' arrays over peer memory;
+ *                  NCCL ranks map each other's arrays with CUDA IPC) (env
+ *                  FALCON_EXCHANGE)
  *   "wl_noq"       WORKLIST dense rounds mark the next bitmap without claims
  *                  or a queue (default 1, env FALCON_WL_NOQ; 0 = off)
+ *   "dl_noq"       the same for DELTA dense rounds (near targets marked, far
+ *                  ones parked; default 1, env FALCON_DL_NOQ)
+ *   "split_div"    DELTA with auto Δ: a near round that hands on more than
+ *                  n / split_div items halves the bucket; items at or beyond
+ *                  the new threshold go back to the far set (env
+ *                  FALCON_SPLIT_DIV; 0 = never)
  *   "local"        SSSP DELTA sparse rounds: each warp expands the in-bucket
  *                  targets it improved itself, up to this many 32-item tiles
  *                  per round, before handing the rest to the next round's

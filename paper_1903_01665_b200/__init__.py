@@ -17,7 +17,7 @@ import os
 
 __all__ = ["load", "graph_load_csr", "graph_free", "graph_info", "graph_share", "falcon_run_many", "falcon_mst", "falcon_trim_memory", "graph_exchange_bytes", "falcon_sssp", "falcon_bfs", "falcon_cc",
            "falcon_set_profiling", "falcon_set_delta", "falcon_set_option", "falcon_partition", "falcon_comm_unique_id",
-           "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_free", "graph_owned_range", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
+           "falcon_comm_init", "falcon_comm_init_simulated", "falcon_comm_loopback_id", "falcon_comm_free", "graph_owned_range", "graph_partition_info", "LOAD_SLICE", "LOAD_GATHER", "Comm", "falcon_last_error", "falcon_version", "FalconError", "FalconStats",
            "STYLES", "INF", "LIB_PATH"]
 
 INF = 2147483647
@@ -25,6 +25,8 @@ STYLE_VERTEX, STYLE_EDGE, STYLE_WORKLIST, STYLE_DELTA = 0, 1, 2, 3
 STYLES = {"vertex": STYLE_VERTEX, "edge": STYLE_EDGE, "worklist": STYLE_WORKLIST, "delta": STYLE_DELTA}
 LOAD_BUILD_COO = 0x1
 LOAD_BUILD_REVERSE = 0x2
+LOAD_SLICE = 0x4    # partitioned: this rank passes only its rows (include/falcon.h)
+LOAD_GATHER = 0x8   # partitioned: full output on every rank (default: the owned slice)
 ALGOS = {"sssp": 0, "bfs": 1, "cc": 2}
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "NO_MEMORY", 4: "CUDA", 5: "OVERFLOW",
           6: "NOT_CONVERGED", 7: "COMM", 8: "UNSUPPORTED"}
@@ -103,7 +105,7 @@ def load(build_if_missing: bool = False):
                                     ctypes.POINTER(FalconStats)]
     lib.falcon_run_many.restype = st
     for f in (lib.falcon_partition, lib.falcon_comm_unique_id, lib.falcon_comm_init, lib.falcon_comm_init_simulated,
-              lib.falcon_comm_free, lib.graph_owned_range):
+              lib.falcon_comm_free, lib.graph_owned_range, lib.falcon_comm_loopback_id, lib.graph_partition_info):
         f.restype = st
     for f in (lib.graph_load_csr, lib.graph_free, lib.graph_info, lib.falcon_sssp, lib.falcon_bfs, lib.falcon_cc,
               lib.falcon_set_profiling):
@@ -229,6 +231,21 @@ def falcon_comm_init(nranks: int, rank: int, unique_id: bytes, device: int) -> C
     return Comm(out, nranks, rank)
 
 
+def falcon_comm_loopback_id(nranks: int) -> bytes:
+    """Id of an in-process loopback world of nranks ranks (host threads of this
+    process; include/falcon.h): pass it to falcon_comm_init from each thread."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().falcon_comm_loopback_id(nranks, ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def graph_partition_info(g: "Graph"):
+    """(exchange mode 1 dense / 2 sparse / 3 fused, supersteps, host round trips) of the last call."""
+    mode, steps, checks = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+    _check(load().graph_partition_info(g.handle, ctypes.byref(mode), ctypes.byref(steps), ctypes.byref(checks)))
+    return mode.value, steps.value, checks.value
+
+
 def falcon_comm_init_simulated(nparts: int) -> Comm:
     out = ctypes.c_void_p()
     _check(load().falcon_comm_init_simulated(nparts, ctypes.byref(out)))
@@ -265,6 +282,10 @@ def graph_load_csr(n: int, m: int, row_off, col, w=None, device: int = -1, strea
     _check(lib.graph_load_csr(n, m, _ptr(row_off), _ptr(col), _ptr(w), ctypes.byref(opts), ctypes.byref(out)))
     g = Graph(out, n, m)
     g._comm = comm   # keep the communicator alive as long as the graph
+    if comm is not None:   # a slice load's n / m are the rank's; the graph's are global
+        g.n, g.m = graph_info(g)
+        lo, hi = graph_owned_range(g)
+        g.out_len = g.n if flags & LOAD_GATHER else hi - lo
     return g
 
 

@@ -179,6 +179,7 @@ struct falcon_graph {
     uint32_t dense_div = 32;             // dense round: frontier > n / dense_div (FALCON_DENSE_DIV; swept 8-128)
     uint32_t blk_div = 8;                // blocked round: frontier > n / blk_div (FALCON_BLOCK_DIV)
     uint32_t wl_noq = 1;                 // WORKLIST dense rounds without claims / queue (FALCON_WL_NOQ)
+    uint32_t dl_noq = 1;                 // ... DELTA dense rounds (FALCON_DL_NOQ)
     // SSSP DELTA sparse rounds: local continuation tiles per warp, in rounds of
     // at most local_max items (FALCON_LOCAL / FALCON_LOCAL_MAX; set at load:
     // 16 / unbounded on sparse high-diameter graphs (m < 3n), 4 / 16384 below
@@ -195,6 +196,8 @@ struct falcon_graph {
     bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
+    uint32_t split_div = 0;              // DELTA (auto Δ): halve the bucket when a near round hands on > n / split_div
+                                         // items (FALCON_SPLIT_DIV; 0 = never)
     int32_t *val = nullptr;
     uint32_t *bm = nullptr, *fr0 = nullptr, *fr1 = nullptr;   // bm: 4 bitmaps of nwords
     uint32_t *tiles = nullptr;           // scan tile sums (load-time layout builds)
@@ -248,6 +251,9 @@ struct falcon_graph {
     uint2 **d_outboxes = nullptr;
     uint32_t **d_counts = nullptr;
     uint32_t exchange = 0;                // 0 auto, 1 dense, 2 sparse, 3 fused (FALCON_EXCHANGE / option "exchange")
+    bool gather = false;                  // (partitioned) FALCON_LOAD_GATHER: full output on every rank
+    uint32_t last_mode = 0;               // (partitioned) exchange mode of the last call (1 dense, 2 sparse, 3 fused)
+    int64_t last_rounds = 0, last_host_checks = 0;   // (partitioned) supersteps / host round trips of the last call
     int32_t **d_peer_val = nullptr;       // (partitioned, fused) every part's value array / bitmaps
     uint32_t **d_peer_bm = nullptr;
     std::vector<void *> ipc_opened;       // (NCCL, fused) peer mappings to close
@@ -268,6 +274,7 @@ struct falcon_graph {
         a.dense_div = dense_div;
         a.blk_div = blk_div;
         a.wl_noq = wl_noq;
+        a.dl_noq = dl_noq;
         a.local_tiles = local_tiles;
         a.local_max = local_max;
         a.wl_local_tiles = wl_local_tiles;
@@ -370,7 +377,7 @@ struct Round {
             if (tr) tr->mark(s, "expand", 0);
         } else if (STYLE == DELTA) {
             if (g->persist) {   // small rounds inside one cooperative kernel
-                launch_coop(g, k_persist<SSSP, DELTA, BLOCK, UNROLL>, g->grid_persist, s, a, g->pull_div, g->persist_max);
+                launch_coop(g, k_persist<SSSP, DELTA, BLOCK, UNROLL>, g->grid_persist, s, a, g->split_div, g->persist_max);
                 launches++;
             }
             // the far-set refill (MODE_SCAN rounds) runs inside the expansion kernel
@@ -392,8 +399,8 @@ struct Round {
         }
         launches++;
         launches++;
-        k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n, g->pull_div,
-                                                 g->blk_div);
+        k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n,
+                                                 STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
     }
@@ -1081,6 +1088,8 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (const char *bmb = getenv("FALCON_BLOCK_MB")) g->blk_bytes = (size_t)atoll(bmb) << 20;   // 0: no blocking
     if (const char *dd = getenv("FALCON_DENSE_DIV")) g->dense_div = (uint32_t)atoi(dd);        // 0: never dense
     if (const char *wq = getenv("FALCON_WL_NOQ")) g->wl_noq = (uint32_t)atoi(wq);
+    if (const char *dq = getenv("FALCON_DL_NOQ")) g->dl_noq = (uint32_t)atoi(dq);
+    if (const char *sd = getenv("FALCON_SPLIT_DIV")) g->split_div = (uint32_t)atoi(sd);
     if (m < 3 * n) { g->local_tiles = 16; g->local_max = 0xffffffffu; g->wl_local_tiles = 4; }
     else if (m >= 6 * n) g->local_tiles = 0;   // dense / skewed (rmat): measured no gain
     if (const char *lt = getenv("FALCON_WL_LOCAL")) g->wl_local_tiles = (uint32_t)atoi(lt);
@@ -1165,7 +1174,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->rowb = p->rowb; v->srcb = p->srcb; v->cwb = p->cwb;
     v->chunk = p->chunk; v->chunkb = p->chunkb; v->chunks = p->chunks;
     v->nblk = p->nblk; v->bsz = p->bsz; v->blk_bytes = p->blk_bytes;
-    v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
+    v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->dl_noq = p->dl_noq; v->split_div = p->split_div; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
     v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
     v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div;
@@ -1210,11 +1219,15 @@ falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, co
                                const falcon_load_opts_t *opts, falcon_graph_t **out) {
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
-    if (n < 1 || n >= (1ll << 31)) return fail(FALCON_ERR_INVALID_ARG, "n must be in [1, 2^31)");
+    const bool slice = opts && (opts->flags & FALCON_LOAD_SLICE);   // a rank's slice may be empty
+    if (n < (slice ? 0 : 1) || n >= (1ll << 31)) return fail(FALCON_ERR_INVALID_ARG, "n must be in [1, 2^31)");
     if (m < 0 || m >= (1ll << 32)) return fail(FALCON_ERR_INVALID_ARG, "m must be in [0, 2^32)");
     if (!row_off || (m > 0 && !col)) return fail(FALCON_ERR_INVALID_ARG, "row_off/col is NULL");
-    if (opts && (opts->flags & ~(uint32_t)(FALCON_LOAD_BUILD_COO | FALCON_LOAD_BUILD_REVERSE)))
+    if (opts && (opts->flags & ~(uint32_t)(FALCON_LOAD_BUILD_COO | FALCON_LOAD_BUILD_REVERSE | FALCON_LOAD_SLICE |
+                                           FALCON_LOAD_GATHER)))
         return fail(FALCON_ERR_UNSUPPORTED, "unknown load flags 0x%x", opts->flags);
+    if (opts && !opts->comm && (opts->flags & (FALCON_LOAD_SLICE | FALCON_LOAD_GATHER)))
+        return fail(FALCON_ERR_INVALID_ARG, "FALCON_LOAD_SLICE / FALCON_LOAD_GATHER need a communicator");
     falcon_graph *g = new (std::nothrow) falcon_graph();
     if (!g) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
     falcon_status_t st = (opts && opts->comm) ? load_partitioned(n, m, row_off, col, w, opts, g)
@@ -1304,6 +1317,16 @@ falcon_status_t graph_exchange_bytes(const falcon_graph_t *g, int64_t *bytes) {
     return FALCON_OK;
 }
 
+falcon_status_t graph_partition_info(const falcon_graph_t *g, int32_t *exchange_mode, int64_t *supersteps,
+                                     int64_t *host_checks) {
+    if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
+    if (!g->comm) return fail(FALCON_ERR_UNSUPPORTED, "not a partitioned graph");
+    if (exchange_mode) *exchange_mode = (int32_t)g->last_mode;
+    if (supersteps) *supersteps = g->last_rounds;
+    if (host_checks) *host_checks = g->last_host_checks;
+    return FALCON_OK;
+}
+
 falcon_status_t graph_owned_range(const falcon_graph_t *g, int64_t *lo, int64_t *hi) {
     if (!g) return fail(FALCON_ERR_INVALID_ARG, "graph is NULL");
     if (lo) *lo = g->comm ? g->lo : 0;
@@ -1327,15 +1350,27 @@ falcon_status_t falcon_comm_unique_id(void *id128) {
     return FALCON_OK;
 }
 
+falcon_status_t falcon_comm_loopback_id(int nranks, void *id128) {
+    if (!id128 || nranks < 1 || nranks > 64) return fail(FALCON_ERR_INVALID_ARG, "nranks must be in [1, 64]");
+    LbWorld *w = new (std::nothrow) LbWorld(nranks);
+    if (!w) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    memset(id128, 0, NCCL_UNIQUE_ID_BYTES);
+    memcpy(id128, LB_MAGIC, 8);
+    memcpy(static_cast<char *>(id128) + 8, &w, sizeof w);
+    return FALCON_OK;
+}
+
 falcon_status_t falcon_comm_init(int nranks, int rank, const void *id128, int device, falcon_comm_t **out) {
     if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return fail(FALCON_ERR_INVALID_ARG, "bad comm arguments");
     *out = nullptr;
-    NcclApi *nc = nccl_api();
+    const bool loop = memcmp(id128, LB_MAGIC, 8) == 0;
+    NcclApi *nc = loop ? loopback_api() : nccl_api();
     if (!nc) return fail(FALCON_ERR_COMM, "libnccl.so.2 could not be loaded");
     CU(cudaSetDevice(device));
     falcon_comm *cm = new (std::nothrow) falcon_comm();
     if (!cm) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
     cm->nranks = nranks; cm->rank = rank; cm->device = device;
+    cm->api = nc; cm->loopback = loop;
     ncclUniqueId id;
     memcpy(&id, id128, sizeof id);
     ncclResult_t r = nc->CommInitRank(&cm->nccl, nranks, id, rank);
@@ -1359,7 +1394,7 @@ falcon_status_t falcon_comm_init_simulated(int nparts, falcon_comm_t **out) {
 
 falcon_status_t falcon_comm_free(falcon_comm_t *cm) {
     if (!cm) return FALCON_OK;
-    if (cm->nccl && nccl_api() && nccl_api()->CommDestroy) nccl_api()->CommDestroy(cm->nccl);
+    if (cm->nccl && cm->api && cm->api->CommDestroy) cm->api->CommDestroy(cm->nccl);
     delete cm;
     return FALCON_OK;
 }
@@ -1420,6 +1455,10 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             g->exchange = (uint32_t)value;
         } else if (!strcmp(name, "wl_noq")) {
             t->wl_noq = (uint32_t)(value != 0);
+        } else if (!strcmp(name, "dl_noq")) {
+            t->dl_noq = (uint32_t)(value != 0);
+        } else if (!strcmp(name, "split_div")) {
+            t->split_div = (uint32_t)value;
         } else if (!strcmp(name, "local")) {
             t->local_tiles = (uint32_t)value;
         } else if (!strcmp(name, "bfs_unit")) {

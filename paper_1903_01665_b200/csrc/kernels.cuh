@@ -33,6 +33,7 @@ constexpr int32_t INF = 0x7fffffff;   // MAX_INT
 __device__ int fk_probe_mode;   // tools/expand_probe.cu only (never defined in the product build)
 #endif
 constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t NONE = 0xffffffffu;   // "no item / no vertex"
 
 enum Algo : int { SSSP = 0, BFS = 1, CC = 2 };
 enum Style : int { VERTEX = 0, EDGE = 1, WORKLIST = 2, DELTA = 3,
@@ -70,10 +71,11 @@ struct Ctrl {
     uint32_t bar_gen;     // persistent kernel: barrier generation
     uint32_t blk;         // this round expands over the destination-blocked layout (dense rounds)
     uint32_t noq;         // WORKLIST: this (dense) round marks the bitmap only -- no queue is built
-    uint32_t prevnoq;     // WORKLIST: the previous round did: read this round's items from the bitmap
+    uint32_t prevnoq;     // WORKLIST / DELTA: the previous round did: read this round's items from the bitmap
     uint32_t hooks;       // MST: components hooked this round
     uint32_t cand_ovf;    // SSSP: some candidate d[u]+w reached INF (k_overflow_check decides, reading R3)
     unsigned long long wsum;       // MST: total weight of the forest edges chosen so far
+    unsigned long long xremote;    // fused partitioned rounds: improvements sent to other parts (RED pairs)
     unsigned long long launches;   // kernels launched by the fixpoint loop
     unsigned long long vertices;   // filled by k_finish
     unsigned long long edges;
@@ -100,6 +102,7 @@ struct Args {
     uint32_t dense_div;        // a round is dense when its frontier exceeds n / dense_div (0: never)
     uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
+    uint32_t dl_noq;           // ... DELTA dense rounds (near marks in the bitmap, far parking as usual)
     // fused partitioned rounds (VFUSED): owned range, part bounds and the
     // owners' value arrays / round bitmaps (peer memory on real GPUs)
     uint32_t lo, hi, nparts;
@@ -290,6 +293,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->delta0 = delta; c->delta_adapt = a.delta_adapt; c->bk_rounds = 0; c->bk_items = 0;
         c->delta_cap = a.delta_cap ? a.delta_cap : 128u;
         c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0; c->cand_ovf = 0;
+        c->xremote = 0;
         if (ALGO != CC) a.fr0[0] = source;
     }
 }
@@ -384,10 +388,16 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
         bool found = false;
         if (v < a.n && !((visw >> lane) & 1u)) {
             nv++;
+            // in-arcs four at a time: four independent column loads, then four
+            // independent bit tests -- two dependent steps per four arcs
             const uint32_t e1 = ld_ro(a.rin_off + v + 1);
-            for (uint32_t e = ld_ro(a.rin_off + v); e < e1; e++) {
-                ne++;
-                if (bit_test(bm_prev, ld_ro(a.rin_col + e))) { found = true; break; }
+            for (uint32_t e = ld_ro(a.rin_off + v); e < e1 && !found; e += 4) {
+                uint32_t cu[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) cu[q] = e + q < e1 ? ld_ro(a.rin_col + e + q) : NONE;
+#pragma unroll
+                for (int q = 0; q < 4; q++) found |= cu[q] != NONE && bit_test(bm_prev, cu[q]);
+                ne += e1 - e < 4 ? e1 - e : 4;
             }
         }
         const unsigned mask = __ballot_sync(FULL, found);
@@ -453,8 +463,6 @@ __device__ __forceinline__ int32_t ld_value(const int32_t *p, uint64_t pl) {
     if (COHERENT) return __ldcg(p);
     return ld_val(p, pl);
 }
-
-constexpr uint32_t NONE = 0xffffffffu;
 
 // Per-round, per-warp expansion state.
 struct Xw {
@@ -533,41 +541,42 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
     }
 #endif
     if constexpr (STYLE == VFUSED) {
-        // Fused partitioned round (SURVEY §8(e) stretch): a target owned by
-        // another part is gathered from, lowered in and marked in THAT part's
-        // value array and round bitmap -- through peer memory on real GPUs --
-        // so no exchange step follows the relax.
+        // Fused partitioned round (SURVEY §8(e) "B200-native stretch"): the
+        // relax kernel is the exchange.  Every target is filtered against
+        // this part's OWN full-length value array (owned range: the values;
+        // elsewhere: the smallest proposal this part has made -- a local
+        // gather, never a remote one), lowered there, and a target owned by
+        // another part also gets the proposal as a fire-and-forget RED.MIN
+        // into the owner's value array and a RED.OR into the owner's round
+        // bitmap -- over NVLink peer memory on real GPUs, device pointers when
+        // simulated / loopback.  No exchange step or apply kernel follows.
+        // A proposal the owner already beats only costs a redundant RED.
         static_assert(ALGO == SSSP, "fused rounds run SSSP (BFS as unit-weight SSSP)");
-        int32_t *tv[U];
-        uint32_t *tb[U];
         int32_t cur[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) cur[q] = s.ok[q] ? ld_value<COHERENT>(a.val + s.v[q], x.pl) : 0;
         const size_t boff = (size_t)(x.bm_now - a.bm0);   // this round's bitmap inside every part's bitmaps
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            tv[q] = a.val; tb[q] = x.bm_now; cur[q] = 0;
             if (!s.ok[q]) continue;
             const uint32_t v = s.v[q];
-            if (v < a.lo || v >= a.hi) {
+            const uint32_t cand = s.p[q] + (uint32_t)s.wt[q];
+            if (cand >= (uint32_t)INF) { acc.ovf = true; continue; }
+            if ((int32_t)cand >= cur[q]) continue;
+            atomicMin(a.val + v, (int32_t)cand);   // owned value or local shadow
+            if (v >= a.lo && v < a.hi) {
+                atomicOr(x.bm_now + (v >> 5), 1u << (v & 31));
+            } else {
                 int lo = 0, hi = (int)a.nparts;   // owner: largest o with bounds[o] <= v
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
                     if (a.bounds[mid] <= v) lo = mid; else hi = mid;
                 }
-                tv[q] = a.peer_val[lo];
-                tb[q] = a.peer_bm[lo] + boff;
+                atomicMin(a.peer_val[lo] + v, (int32_t)cand);
+                atomicOr(a.peer_bm[lo] + boff + (v >> 5), 1u << (v & 31));
+                x.qn++;   // remote improvements of this lane (Ctrl::xremote)
             }
-            cur[q] = __ldcg(tv[q] + v);
-        }
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            if (!s.ok[q]) continue;
-            const uint32_t cand = s.p[q] + (uint32_t)s.wt[q];
-            if (cand >= (uint32_t)INF) { acc.ovf = true; continue; }
-            if ((int32_t)cand < cur[q]) {
-                atomicMin(tv[q] + s.v[q], (int32_t)cand);
-                atomicOr(tb[q] + (s.v[q] >> 5), 1u << (s.v[q] & 31));
-                acc.nu++; acc.chg = true;
-            }
+            acc.nu++; acc.chg = true;
         }
     } else {
     int32_t cur[U];
@@ -619,6 +628,10 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
 #pragma unroll
             for (int q = 0; q < U; q++)
                 if (need[q]) atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));
+            if (STYLE == DELTA) {   // no-queue DELTA round: count the near marks (bucket continues iff > 0)
+#pragma unroll
+                for (int q = 0; q < U; q++) x.qn += (uint32_t)__popc(__ballot_sync(FULL, need[q]));
+            }
         }
     } else if (LOCAL) {
         static_assert(!LOCAL || ALGO == SSSP, "local continuation is min-relaxation (SSSP)");
@@ -675,6 +688,12 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
         }
     }
     }   // STYLE != VFUSED
+}
+
+// DELTA: an item at or beyond the (split) bucket threshold goes back to the far set.
+__device__ __forceinline__ void park_far(const Args &a, Xw &x, uint32_t u, uint32_t d) {
+    atomicOr(a.vis + (u >> 5), 1u << (u & 31));
+    x.pend_min = d < x.pend_min ? d : x.pend_min;
 }
 
 // Relax the arcs of one 32-item tile (lane: value pay, arcs [beg, beg+deg)).
@@ -798,6 +817,10 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                         if (ALGO == BFS && is_vertex(STYLE)) a.val[u] = (int32_t)x.lev;   // discovered last round
                     }
                     if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
+                    if (STYLE == DELTA && u != NONE && pay >= x.thr) {   // bucket was split: back to the far set
+                        if (first) park_far(a, x, u, pay);
+                        deg = 0;
+                    }
                     relax_tile<ALGO, STYLE, U, COHERENT, NOQ>(a, x, beg, deg, pay, acc, pend);
                 }
                 __syncwarp();
@@ -819,6 +842,10 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                 if (QUEUE && last && u != NONE) x.bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
                 if (u != NONE && first) acc.nv++;
                 if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
+                if (STYLE == DELTA && u != NONE && pay >= x.thr) {   // bucket was split: back to the far set
+                    if (first) park_far(a, x, u, pay);
+                    deg = 0;
+                }
                 relax_tile<ALGO, STYLE, U, COHERENT, NOQ, LOCAL>(a, x, beg, deg, pay, acc, pend);
             }
         }
@@ -860,6 +887,15 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
             __syncwarp();
         }
     }
+    if (STYLE == VFUSED) {   // remote improvements sent this round, one atomic per warp
+        unsigned long long r = x.qn;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(FULL, r, o);
+        if (lane == 0 && r) atomicAdd(&c->xremote, r);
+    }
+    if (STYLE == DELTA && NOQ) {   // near marks of a no-queue round: the next round's frontier size (upper bound)
+        if (lane == 0 && x.qn) atomicAdd(&c->out_len, x.qn);
+    }
     if (STYLE == DELTA) {   // warp-min, one atomicMin per warp
         uint32_t pm = x.pend_min;
 #pragma unroll
@@ -896,15 +932,16 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     __shared__ uint32_t s_q[B / 32][WQ];
     __shared__ uint32_t s_it[B / 32][1024];
     RoundAcc acc;
-    if (STYLE == WORKLIST && dense && a.wl_noq) {
-        // dense WORKLIST round: items from the bitmap, improved vertices marked
-        // in the next bitmap with reductions -- no claim atomics, no queue.  The
+    if ((STYLE == WORKLIST && dense && a.wl_noq) || (STYLE == DELTA && dense && a.dl_noq)) {
+        // dense WORKLIST / DELTA round: items from the bitmap, improved vertices
+        // marked in the next bitmap with reductions -- no claim atomics, no
+        // queue (DELTA: near targets only; far ones are parked as usual).  The
         // next round reads its items from that bitmap (Ctrl::prevnoq); if it is
         // sparse, it builds the queue again with claims.
         if (blockIdx.x == 0 && threadIdx.x == 0) c->noq = 1;
         expand_round<ALGO, STYLE, U, false, true>(a, c, iter, thr, in, out, nitems, true, blocked,
                                                   s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
-    } else if (ALGO == SSSP && (STYLE == DELTA ? a.local_tiles && nitems <= a.local_max
+    } else if (ALGO == SSSP && (STYLE == DELTA ? a.local_tiles && nitems <= a.local_max && !c->prevnoq
                                                : a.wl_local_tiles && nitems <= a.wl_local_max && !c->prevnoq) &&
                !dense && !blocked) {
         // sparse SSSP rounds with local continuation (expand_round)
@@ -913,9 +950,10 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
             STYLE == DELTA ? a.local_tiles : a.wl_local_tiles);
     } else {
         expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems,
-                                            dense || (STYLE == WORKLIST && c->prevnoq), blocked,
+                                            dense || ((STYLE == WORKLIST || STYLE == DELTA) && c->prevnoq), blocked,
                                             s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
     }
+    if (STYLE == VFUSED) __threadfence_system();   // remote REDs performed before the termination collective
     flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
 }
 
@@ -1131,9 +1169,11 @@ __global__ void k_compress(Args a) {
 // Decides on the device whether another round runs ("if
 // (changed == 0) break" / SPEC.md:221 "worklist non-empty"), and drives the
 // CUDA-graph WHILE node through cudaGraphSetConditional.
+// aux_div: BFS VERTEX: pull_div (bottom-up threshold); DELTA: split_div (bucket split)
 template <int ALGO, int STYLE>
-__device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t pull_div,
+__device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t aux_div,
                                              uint32_t blk_div) {
+    const uint32_t pull_div = aux_div;
     if (c->done) return false;
     c->launches += launches_per_round;
     bool more = STYLE == WORKLIST ? (c->noq ? c->changed != 0 : c->out_len > 0) : c->changed != 0;
@@ -1169,11 +1209,21 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
                 c->thr = t > 0x7fffffffull ? 0x7fffffffu : (uint32_t)t;
                 c->minpend = 0xffffffffu;   // recomputed by the far scan and later parkings
                 c->mode = MODE_SCAN;
+                c->noq = 0;                 // the refill round builds a queue
             }
         } else {
             more = true;
             c->bk_items += c->in_len;   // a near round of the current bucket
             c->bk_rounds++;
+            // bucket split (aux_div = DELTA's split_div): a near round that
+            // hands on more than n / split_div items relaxes many vertices
+            // before their final value is known -- halve the bucket (not below
+            // the initial width); items of the next round at or above the new
+            // threshold are parked in the far set when loaded (expand_round)
+            if (c->delta_adapt && aux_div && c->out_len > n / aux_div && c->delta / 2u >= c->delta0) {
+                c->delta /= 2u;
+                c->thr -= c->delta;
+            }
         }
     }
     if (c->status != ST_OK) more = false;
@@ -1261,7 +1311,7 @@ __global__ void __launch_bounds__(B, 2) k_persist(Args a, uint32_t pull_div, uin
         if (ldv(&c->done)) break;
         const bool scan = STYLE == DELTA && ldv(&c->mode) == MODE_SCAN;
         if (!scan && ldv(&c->in_len) > max_items) break;
-        if (STYLE == WORKLIST && ldv(&c->prevnoq)) break;   // frontier only in the bitmap: k_expand_warp
+        if ((STYLE == WORKLIST || STYLE == DELTA) && ldv(&c->prevnoq)) break;   // frontier only in the bitmap
         const uint32_t iter = ldv(&c->iter), sel = ldv(&c->sel);
         const uint32_t thr = STYLE == DELTA ? ldv(&c->thr) : 0xffffffffu;
         const uint32_t *in = sel ? a.fr1 : a.fr0;

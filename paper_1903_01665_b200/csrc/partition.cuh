@@ -2,41 +2,43 @@
 // SURVEY.md §8(e)).  Included by falcon.cu (needs falcon_graph, load, run).
 //
 // Part q owns vertices [bounds[q], bounds[q+1]) -- contiguous ranges chosen
-// by EDGE count (binary search on the row_off prefix) -- and stores the CSR
-// rows of its owned vertices only (global column ids), plus a full-length
-// value array: the owned range is authoritative, the rest holds this part's
-// proposals for remote vertices (the "shadow").  A superstep:
+// by EDGE count (binary search on the row_off prefix), or the slices the
+// ranks pass (FALCON_LOAD_SLICE) -- and stores the CSR rows of its owned
+// vertices only (global column ids), plus a full-length value array: the
+// owned range is authoritative, the rest holds this part's proposals for
+// remote vertices (the "shadow").  A superstep:
 //   1. relax: the single-GPU VERTEX round (k_expand_warp) over the
 //      part's rows; MIN lands in the local full-length array;
-//   2. exchange: every owner receives the MIN over all parts of its range
-//      (grouped ncclReduce(ncclMin), one per owner -- volume 4n(P-1)/P per
-//      rank, the reduce-scatter of SURVEY §8(e));
-//   3. apply: owned values improved by a remote proposal are lowered and
-//      marked active;
-//   4. termination: ncclAllReduce(SUM) of the per-part `changed` flag, then
+//   2. exchange, one of
+//      - fused (the default between ranks): the relax kernel itself sends
+//        every remote improvement as a RED.MIN + bitmap RED.OR into the
+//        owner's arrays over peer memory (NVLink; CUDA IPC mappings), so no
+//        exchange step follows;
+//      - dense: every owner receives the MIN over all parts of its range
+//        (grouped ncclReduce(ncclMin), one per owner -- volume 4n(P-1)/P per
+//        rank, the reduce-scatter of SURVEY §8(e)), then applies it;
+//      - sparse: (vertex, value) pairs of the remote improvements, grouped
+//        ncclSend / ncclRecv after a count exchange (host-synchronised per
+//        superstep: the payload sizes are host arguments);
+//   3. termination: ncclAllReduce(SUM) of the per-part `changed` flag, then
 //      the usual device-side advance -- every part takes the same decision.
+//      The host looks at the control block once every HOST_CHECK_EVERY
+//      supersteps (fused and dense rounds have no per-superstep host sync).
 // MIN is associative, commutative and idempotent, so any partition and any
 // exchange schedule reach the same unique fixpoint: results are bit-identical
-// to one GPU (tests: simulated P parts on one device, tests/test_partition*).
-// BFS runs as unit-weight SSSP (hop distance = level).  CC hooks on a
-// replicated label array: local union-find pass, ncclAllReduce(MIN) of the
-// parent array, pointer jumping, until no part hooks (the set of roots only
-// shrinks, so it terminates).
+// to one GPU.  BFS runs as unit-weight SSSP (hop distance = level).  CC hooks
+// on a replicated label array: local union-find pass, ncclAllReduce(MIN) of
+// the parent array, pointer jumping, until no part hooks.
 //
-// "Simulated" communicators run all P parts on the current device in one
-// process with the exchange done by device kernels -- the same partition,
-// relax, apply and termination code -- so the partitioned algorithm is
-// tested on one GPU.  NCCL is bound at run time (dlopen libnccl.so.2): a
-// single-GPU user never needs it.
+// Communicators: NCCL ranks (one process per GPU; libnccl bound at run time
+// with dlopen, so single-GPU users never need it); LOOPBACK ranks (host
+// threads of one process sharing a device, loopback.cuh: the same per-rank
+// code with the NCCL calls served in-process -- how the rank path is tested
+// on a one-GPU box); SIMULATED communicators (one handle runs all P parts on
+// one device with device-kernel exchanges).
 #pragma once
 #include <dlfcn.h>
 #include <nccl.h>
-
-struct falcon_comm {
-    int nranks = 1, rank = 0, device = 0;
-    int simulated = 0;            // > 0: number of parts simulated on one device
-    ncclComm_t nccl = nullptr;
-};
 
 namespace {
 
@@ -80,12 +82,43 @@ NcclApi *nccl_api() {
     return &api;
 }
 
-#define NC(call)                                                                                   \
-    do {                                                                                           \
-        ncclResult_t _r = (call);                                                                  \
-        if (_r != ncclSuccess)                                                                     \
-            return fail(FALCON_ERR_COMM, "%s: %s", #call,                                          \
-                        nccl_api()->GetErrorString ? nccl_api()->GetErrorString(_r) : "nccl error"); \
+}  // namespace
+
+#include "loopback.cuh"
+
+struct falcon_comm {
+    int nranks = 1, rank = 0, device = 0;
+    int simulated = 0;            // > 0: number of parts simulated on one device
+    ncclComm_t nccl = nullptr;
+    NcclApi *api = nullptr;       // libnccl, or the in-process loopback transport
+    bool loopback = false;        // ranks are threads of this process on one device
+};
+
+namespace {
+
+// The loopback transport behind the NCCL function table (loopback.cuh).
+NcclApi *loopback_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        a.h = reinterpret_cast<void *>(1);
+        a.GetUniqueId = lb_GetUniqueId; a.CommInitRank = lb_CommInitRank; a.CommDestroy = lb_CommDestroy;
+        a.Reduce = lb_Reduce; a.AllReduce = lb_AllReduce; a.Broadcast = lb_Broadcast; a.Send = lb_Send;
+        a.Recv = lb_Recv; a.AllGather = lb_AllGather; a.GroupStart = lb_GroupStart; a.GroupEnd = lb_GroupEnd;
+        a.GetErrorString = lb_GetErrorString;
+        return a;
+    }();
+    return &api;
+}
+
+const char *nc_errstr(ncclResult_t r) {
+    NcclApi *a = nccl_api();
+    return a && a->GetErrorString ? a->GetErrorString(r) : lb_GetErrorString(r);
+}
+
+#define NC(call)                                                                                    \
+    do {                                                                                            \
+        ncclResult_t _r = (call);                                                                   \
+        if (_r != ncclSuccess) return fail(FALCON_ERR_COMM, "%s: %s", #call, nc_errstr(_r));        \
     } while (0)
 
 // ------------------------------------------------------------------ kernels
@@ -297,10 +330,12 @@ falcon_status_t ensure_bounds(falcon_graph *g) {
 }
 
 // Peer tables of the fused exchange: every part's value array and round
-// bitmaps.  Simulated parts: plain device pointers.  NCCL ranks: CUDA IPC
-// handles of each rank's arrays, all-gathered over NCCL and opened with
-// peer access (NVLink), so a relax kernel's atomicMin / atomicOr land
-// directly in the owner's memory.
+// bitmaps.  Simulated parts and loopback ranks (one process, one device):
+// plain device pointers (all-gathered between loopback ranks).  NCCL ranks:
+// CUDA IPC handles of each rank's arrays, all-gathered over NCCL and opened
+// with peer access, so a relax kernel's RED.MIN / RED.OR land directly in the
+// owner's memory over NVLink.  A rank that cannot map a peer fails with COMM
+// (auto mode then falls back to the dense exchange).
 falcon_status_t ensure_fused(falcon_graph *g) {
     if (g->d_peer_val) return FALCON_OK;
     falcon_status_t st = ensure_bounds(g);
@@ -312,8 +347,24 @@ falcon_status_t ensure_fused(falcon_graph *g) {
     std::vector<uint32_t *> hb((size_t)P);
     if (cm->simulated) {
         for (int q = 0; q < P; q++) { hv[(size_t)q] = g->parts[(size_t)q]->val; hb[(size_t)q] = g->parts[(size_t)q]->bm; }
+    } else if (cm->loopback) {
+        falcon_graph *me = g->parts[0];
+        uint64_t mine[2] = {(uint64_t)(uintptr_t)me->val, (uint64_t)(uintptr_t)me->bm};
+        uint64_t *d_send = nullptr, *d_all = nullptr;
+        CU(dmalloc(&d_send, 2));
+        CU(dmalloc(&d_all, 2 * (size_t)P));
+        CU(cudaMemcpyAsync(d_send, mine, sizeof mine, cudaMemcpyHostToDevice, s));
+        NC(cm->api->AllGather(d_send, d_all, 2, ncclUint64, cm->nccl, s));
+        std::vector<uint64_t> all(2 * (size_t)P);
+        CU(cudaMemcpyAsync(all.data(), d_all, sizeof(uint64_t) * 2 * P, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        dfree(d_send); dfree(d_all);
+        for (int q = 0; q < P; q++) {
+            hv[(size_t)q] = reinterpret_cast<int32_t *>((uintptr_t)all[2 * (size_t)q]);
+            hb[(size_t)q] = reinterpret_cast<uint32_t *>((uintptr_t)all[2 * (size_t)q + 1]);
+        }
     } else {
-        NcclApi *nc = nccl_api();
+        NcclApi *nc = cm->api;
         if (!nc->AllGather) return fail(FALCON_ERR_COMM, "ncclAllGather unavailable");
         falcon_graph *me = g->parts[0];
         cudaIpcMemHandle_t mine[2];
@@ -331,8 +382,12 @@ falcon_status_t ensure_fused(falcon_graph *g) {
         for (int q = 0; q < P; q++) {
             if (q == cm->rank) { hv[(size_t)q] = me->val; hb[(size_t)q] = me->bm; continue; }
             void *pv = nullptr, *pb = nullptr;
-            CU(cudaIpcOpenMemHandle(&pv, all[(size_t)q * 2], cudaIpcMemLazyEnablePeerAccess));
-            CU(cudaIpcOpenMemHandle(&pb, all[(size_t)q * 2 + 1], cudaIpcMemLazyEnablePeerAccess));
+            if (cudaIpcOpenMemHandle(&pv, all[(size_t)q * 2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+                cudaIpcOpenMemHandle(&pb, all[(size_t)q * 2 + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                if (pv) cudaIpcCloseMemHandle(pv);
+                return fail(FALCON_ERR_COMM, "rank %d cannot map rank %d's memory (no peer access)", cm->rank, q);
+            }
             g->ipc_opened.push_back(pv);
             g->ipc_opened.push_back(pb);
             hv[(size_t)q] = static_cast<int32_t *>(pv);
@@ -377,7 +432,24 @@ falcon_status_t ensure_sparse(falcon_graph *g) {
     return FALCON_OK;
 }
 
-// Build the part owning [lo, hi): its rows only, global ids, full n.
+// The rest of a part once its CSR is loaded: owned range, receive buffer of
+// the dense exchange, unit-weight arcs (BFS as unit-weight SSSP).
+falcon_status_t finish_part(falcon_graph *p, int64_t lo, int64_t hi) {
+    p->lo = lo; p->hi = hi;
+    CU(dmalloc(&p->recv, (size_t)(hi - lo > 0 ? hi - lo : 1)));
+    CU(dmalloc(&p->cw_unit, (size_t)(p->m ? p->m : 1)));
+    if (p->m) {
+        int32_t *ones = nullptr;
+        CU(dmalloc(&ones, (size_t)p->m));
+        k_fill_i32<<<p->num_sms * 8, BLOCK, 0, p->stream>>>(ones, (uint64_t)p->m, 1);
+        k_interleave<<<p->num_sms * 8, BLOCK, 0, p->stream>>>((uint64_t)p->m, p->col, ones, p->cw_unit);
+        CU(cudaStreamSynchronize(p->stream));
+        dfree(ones);
+    }
+    return FALCON_OK;
+}
+
+// Build the part owning [lo, hi) from the FULL CSR: its rows only, global ids, full n.
 falcon_status_t load_part(int64_t n, const uint32_t *h_row_off, const uint32_t *col, const int32_t *w, int64_t lo,
                           int64_t hi, int device, void *stream, falcon_graph **out) {
     std::vector<uint32_t> ro((size_t)n + 1);
@@ -393,19 +465,80 @@ falcon_status_t load_part(int64_t n, const uint32_t *h_row_off, const uint32_t *
     if (!p) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
     const int64_t mp = (int64_t)(top - base);
     falcon_status_t st = load(n, mp, ro.data(), col + base, w ? w + base : nullptr, &o, p);
+    if (st == FALCON_OK) st = finish_part(p, lo, hi);
     if (st != FALCON_OK) { destroy(p); return st; }
-    p->lo = lo; p->hi = hi;
-    CU(dmalloc(&p->recv, (size_t)(hi - lo)));
-    CU(dmalloc(&p->cw_unit, (size_t)(mp ? mp : 1)));
-    if (mp) {
-        int32_t *ones = nullptr;
-        CU(dmalloc(&ones, (size_t)mp));
-        k_fill_i32<<<p->num_sms * 8, BLOCK, 0, p->stream>>>(ones, (uint64_t)mp, 1);
-        k_interleave<<<p->num_sms * 8, BLOCK, 0, p->stream>>>((uint64_t)mp, p->col, ones, p->cw_unit);
-        CU(cudaStreamSynchronize(p->stream));
-        dfree(ones);
-    }
     *out = p;
+    return FALCON_OK;
+}
+
+// Full-length row offsets of a slice part: 0 before lo, the slice's offsets
+// on [lo, hi], m_local after hi (rows outside the slice are empty).
+__global__ void k_slice_rows(uint32_t N, uint32_t lo, uint32_t hi, uint32_t m_local, const uint32_t *slice_ro,
+                             uint32_t *ro) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= N; v += stride)
+        ro[v] = v < lo ? 0u : (v <= hi ? slice_ro[v - lo] : m_local);
+}
+
+// FALCON_LOAD_SLICE: this rank passed only its rows.  The ranks all-gather
+// their (rows, arcs) counts; rank r owns the vertices after those of ranks
+// < r.  The rank's CSR is validated on the device (load) against the global
+// vertex count -- no full-graph host copy or host loop.
+falcon_status_t load_slice(int64_t n_local, int64_t m_local, const uint32_t *row_off, const uint32_t *col,
+                           const int32_t *w, const falcon_load_opts_t *opts, falcon_graph *g) {
+    falcon_comm *cm = opts->comm;
+    const int P = cm->nranks;
+    NcclApi *nc = cm->api;
+    const int device = cm->device;
+    CU(cudaSetDevice(device));
+    cudaStream_t s = nullptr;
+    CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SGuard { cudaStream_t s; ~SGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{s};
+    uint64_t *d_cnt = nullptr;
+    CU(dmalloc(&d_cnt, 2 * (size_t)P + 2));
+    uint64_t mine[2] = {(uint64_t)n_local, (uint64_t)m_local};
+    CU(cudaMemcpyAsync(d_cnt + 2 * P, mine, sizeof mine, cudaMemcpyHostToDevice, s));
+    NC(nc->AllGather(d_cnt + 2 * P, d_cnt, 2, ncclUint64, cm->nccl, s));
+    std::vector<uint64_t> cnt(2 * (size_t)P);
+    CU(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(uint64_t) * 2 * P, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    dfree(d_cnt);
+    uint64_t N = 0, M = 0;
+    g->bounds.assign((size_t)P + 1, 0);
+    for (int q = 0; q < P; q++) {
+        g->bounds[(size_t)q] = (int64_t)N;
+        N += cnt[2 * (size_t)q];
+        M += cnt[2 * (size_t)q + 1];
+    }
+    g->bounds[(size_t)P] = (int64_t)N;
+    if (N < 1 || N >= (1ull << 31)) return fail(FALCON_ERR_INVALID_ARG, "the slices hold %llu vertices (need [1, 2^31))",
+                                                (unsigned long long)N);
+    g->n = (int64_t)N; g->m = (int64_t)M;
+    const int64_t lo = g->bounds[(size_t)cm->rank], hi = g->bounds[(size_t)cm->rank + 1];
+    // the slice's first and last offsets (host or device pointer)
+    uint32_t ends[2] = {1, 0};
+    CU(cudaMemcpy(&ends[0], row_off, 4, cudaMemcpyDefault));
+    CU(cudaMemcpy(&ends[1], row_off + n_local, 4, cudaMemcpyDefault));
+    if (ends[0] != 0 || ends[1] != (uint64_t)m_local)
+        return fail(FALCON_ERR_OUT_OF_RANGE, "slice row_off must start at 0 and end at m");
+    uint32_t *d_slice = nullptr, *d_ro = nullptr;
+    CU(dmalloc(&d_slice, (size_t)n_local + 1));
+    CU(dmalloc(&d_ro, (size_t)N + 1));
+    CU(cudaMemcpyAsync(d_slice, row_off, ((size_t)n_local + 1) * 4, cudaMemcpyDefault, s));
+    k_slice_rows<<<1184, BLOCK, 0, s>>>((uint32_t)N, (uint32_t)lo, (uint32_t)hi, (uint32_t)m_local, d_slice, d_ro);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s));
+    falcon_load_opts_t o = {};
+    o.device = device;
+    o.cuda_stream = opts->cuda_stream;
+    falcon_graph *p = new (std::nothrow) falcon_graph();
+    if (!p) return fail(FALCON_ERR_NO_MEMORY, "host allocation failed");
+    falcon_status_t st = load((int64_t)N, m_local, d_ro, col, w, &o, p);   // device validation: col < N, w >= 0
+    dfree(d_slice);
+    dfree(d_ro);
+    if (st == FALCON_OK) st = finish_part(p, lo, hi);
+    if (st != FALCON_OK) { destroy(p); return st; }
+    g->parts.push_back(p);
     return FALCON_OK;
 }
 
@@ -413,77 +546,41 @@ falcon_status_t load_partitioned(int64_t n, int64_t m, const uint32_t *row_off, 
                                  const falcon_load_opts_t *opts, falcon_graph *g) {
     falcon_comm *cm = opts->comm;
     g->comm = cm;
-    g->n = n; g->m = m;
+    g->gather = (opts->flags & FALCON_LOAD_GATHER) != 0;
     const int P = cm->simulated ? cm->simulated : cm->nranks;
-    // host copy of the offsets (the caller's may live on the device)
-    std::vector<uint32_t> h_ro((size_t)n + 1);
-    CU(cudaMemcpy(h_ro.data(), row_off, ((size_t)n + 1) * 4, cudaMemcpyDefault));
-    if (h_ro[0] != 0 || h_ro[(size_t)n] != (uint64_t)m)
-        return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must start at 0 and end at m");
-    for (int64_t v = 0; v < n; v++)
-        if (h_ro[(size_t)v] > h_ro[(size_t)v + 1])
-            return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must be nondecreasing");
-    g->bounds.assign((size_t)P + 1, 0);
-    partition_bounds(n, h_ro.data(), P, g->bounds.data());
-    const int device = cm->simulated ? (opts->device >= 0 ? opts->device : 0) : cm->device;
-    g->device = device;
-    CU(cudaSetDevice(device));
-    for (int q = 0; q < P; q++) {
-        if (!cm->simulated && q != cm->rank) continue;
-        falcon_graph *p = nullptr;
-        falcon_status_t st = load_part(n, h_ro.data(), col, w, g->bounds[q], g->bounds[q + 1], device,
-                                       opts->cuda_stream, &p);
+    if (opts->flags & FALCON_LOAD_SLICE) {
+        if (cm->simulated)
+            return fail(FALCON_ERR_UNSUPPORTED, "FALCON_LOAD_SLICE needs a rank communicator (one handle per rank)");
+        falcon_status_t st = load_slice(n, m, row_off, col, w, opts, g);
         if (st != FALCON_OK) return st;
-        g->parts.push_back(p);
+    } else {
+        g->n = n; g->m = m;
+        // host copy of the offsets (the caller's may live on the device)
+        std::vector<uint32_t> h_ro((size_t)n + 1);
+        CU(cudaMemcpy(h_ro.data(), row_off, ((size_t)n + 1) * 4, cudaMemcpyDefault));
+        if (h_ro[0] != 0 || h_ro[(size_t)n] != (uint64_t)m)
+            return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must start at 0 and end at m");
+        for (int64_t v = 0; v < n; v++)
+            if (h_ro[(size_t)v] > h_ro[(size_t)v + 1])
+                return fail(FALCON_ERR_OUT_OF_RANGE, "row_off must be nondecreasing");
+        g->bounds.assign((size_t)P + 1, 0);
+        partition_bounds(n, h_ro.data(), P, g->bounds.data());
+        const int device = cm->simulated ? (opts->device >= 0 ? opts->device : 0) : cm->device;
+        CU(cudaSetDevice(device));
+        for (int q = 0; q < P; q++) {
+            if (!cm->simulated && q != cm->rank) continue;
+            falcon_graph *p = nullptr;
+            falcon_status_t st = load_part(n, h_ro.data(), col, w, g->bounds[q], g->bounds[q + 1], device,
+                                           opts->cuda_stream, &p);
+            if (st != FALCON_OK) return st;
+            g->parts.push_back(p);
+        }
     }
+    g->device = g->parts[0]->device;
     g->lo = cm->simulated ? 0 : g->bounds[cm->rank];
-    g->hi = cm->simulated ? n : g->bounds[cm->rank + 1];
+    g->hi = cm->simulated ? g->n : g->bounds[cm->rank + 1];
     g->stream = g->parts[0]->stream;
     if (const char *ex = getenv("FALCON_EXCHANGE")) g->exchange = (uint32_t)atoi(ex) % 4u;
-    return FALCON_OK;
-}
-
-// Per-owner counts of the remote vertices each part improved this round, and
-// the decision: sparse when their pairs (8 B each) are fewer bytes than the
-// dense exchange (4 n (P-1) bytes over all ranks), or when forced.
-falcon_status_t exchange_counts(falcon_graph *g, const std::vector<Args> &args, cudaStream_t s, bool *sparse) {
-    falcon_comm *cm = g->comm;
-    const int P = cm->simulated ? cm->simulated : cm->nranks;
-    falcon_status_t st = ensure_sparse(g);
-    if (st != FALCON_OK) return st;
-    if (g->exchange == 2) { *sparse = true; return FALCON_OK; }
-    // simulated parts share one device's memory: the dense device-side reduce
-    // costs no interconnect traffic, a per-round decision would only add host
-    // synchronisation -- auto is dense there (sparse stays selectable)
-    if (cm->simulated) { *sparse = false; return FALCON_OK; }
-    unsigned long long total = 0;
-    std::vector<uint32_t> h((size_t)P);
-    for (size_t i = 0; i < g->parts.size(); i++) {
-        falcon_graph *p = g->parts[i];
-        CU(cudaMemsetAsync(p->xcounts, 0, (size_t)P * 4, s));
-        k_remote_pairs<false><<<p->grid_small, BLOCK, 0, s>>>(args[i], (uint32_t)p->lo, (uint32_t)p->hi, g->bounds_d,
-                                                              P, p->xcounts, nullptr);
-    }
-    if (cm->simulated) {
-        for (auto *p : g->parts) {
-            CU(cudaMemcpyAsync(h.data(), p->xcounts, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
-            CU(cudaStreamSynchronize(s));
-            for (int q = 0; q < P; q++) total += h[(size_t)q];
-        }
-    } else {   // the decision must be the same on every rank: all-reduce the local totals
-        NcclApi *nc = nccl_api();
-        falcon_graph *me = g->parts[0];
-        CU(cudaMemcpyAsync(h.data(), me->xcounts, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        unsigned long long local = 0;
-        for (int q = 0; q < P; q++) local += h[(size_t)q];
-        unsigned long long *d_tot = reinterpret_cast<unsigned long long *>(me->xcnt_recv);   // P >= 2 words
-        CU(cudaMemcpyAsync(d_tot, &local, 8, cudaMemcpyHostToDevice, s));
-        NC(nc->AllReduce(d_tot, d_tot, 1, ncclUint64, ncclSum, cm->nccl, s));
-        CU(cudaMemcpyAsync(&total, d_tot, 8, cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-    }
-    *sparse = 8ull * total < 4ull * (uint64_t)g->n * (uint64_t)(P - 1);
     return FALCON_OK;
 }
 
@@ -508,7 +605,7 @@ falcon_status_t exchange_sparse(falcon_graph *g, const std::vector<Args> &args, 
         k_sum_counts<<<1, 64, 0, s>>>(g->d_counts, P, g->xpairs_d);   // bytes moved, read once per call
         return FALCON_OK;
     }
-    NcclApi *nc = nccl_api();
+    NcclApi *nc = cm->api;
     if (!nc->Send || !nc->Recv) return fail(FALCON_ERR_COMM, "ncclSend/ncclRecv unavailable");
     falcon_graph *me = g->parts[0];
     const int r = cm->rank;
@@ -524,13 +621,15 @@ falcon_status_t exchange_sparse(falcon_graph *g, const std::vector<Args> &args, 
     CU(cudaMemcpyAsync(hr.data(), me->xcnt_recv, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     uint64_t in_total = 0;
-    NC(nc->GroupStart());   // payloads: my pairs for q from my outbox region q, q's pairs for me into my inbox
+    // payloads: my pairs for q from my outbox region q, q's pairs for me into
+    // my inbox.  Every pair of ranks exchanges a message, possibly empty, so
+    // every rank takes part in the group (the loopback transport matches whole
+    // groups; NCCL accepts zero-count sends).
+    NC(nc->GroupStart());
     for (int q = 0; q < P; q++) {
         if (q == r) continue;
-        if (hs[(size_t)q])
-            NC(nc->Send(me->outbox + g->bounds[(size_t)q], 2 * (size_t)hs[(size_t)q], ncclUint32, q, cm->nccl, s));
-        if (hr[(size_t)q])
-            NC(nc->Recv(me->inbox + in_total, 2 * (size_t)hr[(size_t)q], ncclUint32, q, cm->nccl, s));
+        NC(nc->Send(me->outbox + g->bounds[(size_t)q], 2 * (size_t)hs[(size_t)q], ncclUint32, q, cm->nccl, s));
+        NC(nc->Recv(me->inbox + in_total, 2 * (size_t)hr[(size_t)q], ncclUint32, q, cm->nccl, s));
         in_total += hr[(size_t)q];
         g->xbytes += 8ull * hs[(size_t)q];
     }
@@ -539,14 +638,36 @@ falcon_status_t exchange_sparse(falcon_graph *g, const std::vector<Args> &args, 
     return FALCON_OK;
 }
 
-// One partitioned call.  The output is the full n-length array on every rank.
+// Gather the full n-array into dst (device): every part's owned range.
+falcon_status_t gather_full(falcon_graph *g, int32_t *dst, cudaStream_t s) {
+    falcon_comm *cm = g->comm;
+    if (cm->simulated) {
+        for (auto *p : g->parts)
+            if (p->hi > p->lo)
+                CU(cudaMemcpyAsync(dst + p->lo, p->val + p->lo, (size_t)(p->hi - p->lo) * 4, cudaMemcpyDefault, s));
+        return FALCON_OK;
+    }
+    NcclApi *nc = cm->api;
+    falcon_graph *me = g->parts[0];
+    NC(nc->GroupStart());
+    for (int q = 0; q < cm->nranks; q++) {
+        const int64_t qlo = g->bounds[(size_t)q], qcnt = g->bounds[(size_t)q + 1] - qlo;
+        if (qcnt == 0) continue;
+        NC(nc->Broadcast(me->val + qlo, dst + qlo, (size_t)qcnt, ncclInt32, q, cm->nccl, s));
+    }
+    NC(nc->GroupEnd());
+    return FALCON_OK;
+}
+
+// One partitioned call.  Output: this rank's owned slice [lo, hi) (NCCL /
+// loopback ranks), the full n-array with FALCON_LOAD_GATHER or simulated.
 falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int32_t *out, falcon_stats_t *stats) {
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "output pointer is NULL");
     if (algo != CC && (int64_t)source >= g->n) return fail(FALCON_ERR_INVALID_ARG, "source %u >= n", source);
     falcon_comm *cm = g->comm;
     const int P = (int)g->parts.size();
-    NcclApi *nc = cm->simulated ? nullptr : nccl_api();
-    if (!cm->simulated && !nc) return fail(FALCON_ERR_COMM, "libnccl.so.2 could not be loaded");
+    NcclApi *nc = cm->simulated ? nullptr : cm->api;
+    if (!cm->simulated && !nc) return fail(FALCON_ERR_COMM, "no communicator transport");
     CU(cudaSetDevice(g->device));
     cudaStream_t s = g->parts[0]->stream;   // simulated parts share the device; order them on one stream
     const uint32_t cap = (uint32_t)(g->n + 2 > 0xFFFFFFF0ll ? 0xFFFFFFF0ll : g->n + 2);
@@ -567,7 +688,12 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         CU(cudaMemcpyAsync(d_vals, hv.data(), sizeof(int32_t *) * P, cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(d_ctrls, hc.data(), sizeof(Ctrl *) * P, cudaMemcpyHostToDevice, s));
     }
-    const bool fused = g->exchange == 3 && algo != CC;
+    // exchange mode: 1 dense, 2 sparse, 3 fused; auto (0) = fused between
+    // ranks that can map each other's memory, else dense
+    uint32_t mode = g->exchange;
+    if (algo == CC) mode = 1;
+    if (mode == 0) mode = cm->simulated ? 1 : (ensure_fused(g) == FALCON_OK ? 3 : 1);
+    const bool fused = mode == 3;
     if (fused) {
         falcon_status_t st = ensure_fused(g);
         if (st != FALCON_OK) return st;
@@ -579,6 +705,7 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
             args[i].bounds = g->bounds_d; args[i].peer_val = g->d_peer_val; args[i].peer_bm = g->d_peer_bm;
         }
     }
+    g_last_error.clear();
     CU(cudaEventRecord(g->parts[0]->ev0, s));
     g->xbytes = 0;
     if (g->xpairs_d) CU(cudaMemsetAsync(g->xpairs_d, 0, 8, s));
@@ -589,7 +716,11 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         else k_init<SSSP><<<p->grid_small, BLOCK, 0, s>>>(args[i], source, cap, 3u * p->cnt_slots, VERTEX, 1);
     }
     CU(cudaGetLastError());
-    int64_t rounds = 0;
+    if (fused && !cm->simulated) {   // every rank's init is complete before any peer writes into it
+        NC(nc->AllReduce(&g->parts[0]->ctrl->changed, &g->parts[0]->ctrl->changed, 1, ncclUint32, ncclSum,
+                         cm->nccl, s));
+    }
+    int64_t rounds = 0, host_checks = 0;
     for (;;) {
         for (int k = 0; k < HOST_CHECK_EVERY; k++) {
             rounds++;
@@ -610,17 +741,17 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
                     k_sim_allreduce_min<<<g->parts[0]->grid_small, BLOCK, 0, s>>>(d_vals, P, (uint32_t)g->n);
                 } else {
                     NC(nc->AllReduce(g->parts[0]->val, g->parts[0]->val, (size_t)g->n, ncclInt32, ncclMin, cm->nccl, s));
+                    g->xbytes += 4ull * (uint64_t)g->n;
                 }
                 for (size_t i = 0; i < g->parts.size(); i++)
                     launch_l2(g->parts[i], k_compress, g->parts[i]->grid_small, s, args[i]);
             } else if (fused) {
                 // nothing to exchange: the relax kernels wrote into the owners
             } else {
-                // dense reduce-scatter or sparse (vertex, value) pairs, decided per round
-                bool sparse = false;
                 const int NP = cm->simulated ? P : cm->nranks;
-                if (g->exchange != 1 && NP > 1) {
-                    falcon_status_t st = exchange_counts(g, args, s, &sparse);
+                const bool sparse = mode == 2 && NP > 1;
+                if (sparse) {
+                    falcon_status_t st = ensure_sparse(g);
                     if (st != FALCON_OK) return st;
                 }
                 if (sparse) {
@@ -666,6 +797,7 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
             }
         }
         CU(cudaGetLastError());
+        host_checks++;   // the only host round trip: once per HOST_CHECK_EVERY supersteps
         CU(cudaMemcpyAsync(g->parts[0]->h_ctrl, g->parts[0]->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
         if (g->parts[0]->h_ctrl->done) break;
@@ -678,58 +810,61 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
         CU(cudaStreamSynchronize(s));
         g->xbytes += 8ull * pairs;
     }
-    // gather: the full array on every rank
-    int32_t *dst = out;
-    int32_t *staging = nullptr;
+    // output: the owned slice, or the full array on every rank
+    const bool full_out = cm->simulated || g->gather;
     cudaPointerAttributes at;
     const bool out_on_device = cudaPointerGetAttributes(&at, out) == cudaSuccess &&
                                (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
     cudaGetLastError();
-    if (!out_on_device) {
-        CU(dmalloc(&staging, (size_t)g->n));
-        dst = staging;
-    }
-    if (cm->simulated) {
-        for (auto *p : g->parts)
-            if (p->hi > p->lo)
-                CU(cudaMemcpyAsync(dst + p->lo, p->val + p->lo, (size_t)(p->hi - p->lo) * 4, cudaMemcpyDefault, s));
-    } else {
-        falcon_graph *me = g->parts[0];
-        NC(nc->GroupStart());
-        for (int q = 0; q < cm->nranks; q++) {
-            const int64_t qlo = g->bounds[(size_t)q], qcnt = g->bounds[(size_t)q + 1] - qlo;
-            if (qcnt == 0) continue;
-            NC(nc->Broadcast(me->val + qlo, dst + qlo, (size_t)qcnt, ncclInt32, q, cm->nccl, s));
-        }
-        NC(nc->GroupEnd());
+    int32_t *full = nullptr, *staging = nullptr;
+    if (full_out) {
+        if (!out_on_device) CU(dmalloc(&staging, (size_t)g->n));
+        full = out_on_device ? out : staging;
+        falcon_status_t st = gather_full(g, full, s);
+        if (st != FALCON_OK) return st;
     }
     CU(cudaEventRecord(g->parts[0]->ev1, s));
-    if (staging) CU(cudaMemcpyAsync(out, staging, (size_t)g->n * 4, cudaMemcpyDeviceToHost, s));
+    if (full_out) {
+        if (staging) CU(cudaMemcpyAsync(out, staging, (size_t)g->n * 4, cudaMemcpyDeviceToHost, s));
+    } else if (g->hi > g->lo) {
+        CU(cudaMemcpyAsync(out, g->parts[0]->val + g->lo, (size_t)(g->hi - g->lo) * 4, cudaMemcpyDefault, s));
+    }
     std::vector<Ctrl> hc(g->parts.size());
     for (size_t i = 0; i < g->parts.size(); i++)
         CU(cudaMemcpyAsync(&hc[i], g->parts[i]->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    if (fused)   // each remote improvement moved a RED.MIN (4 B) and a bitmap RED.OR (4 B) to its owner
+        for (auto &c : hc) g->xbytes += 8ull * c.xremote;
     bool overflow = false;
-    {   // overflow certificate (R3) over every part's rows against the gathered array
+    {   // overflow certificate (R3) over every part's rows against the full array
         uint32_t any = 0;
         for (auto &c : hc) any |= c.cand_ovf;
+        falcon_graph *me = g->parts[0];
         if (!cm->simulated) {   // the same decision on every rank
-            falcon_graph *me = g->parts[0];
             CU(cudaMemcpyAsync(me->d_flags, &any, 4, cudaMemcpyHostToDevice, s));
             NC(nc->AllReduce(me->d_flags, me->d_flags, 1, ncclUint32, ncclMax, cm->nccl, s));
             CU(cudaMemcpyAsync(&any, me->d_flags, 4, cudaMemcpyDeviceToHost, s));
             CU(cudaStreamSynchronize(s));
         }
         if (algo == SSSP && any) {
+            int32_t *arr = full;
+            int32_t *tmp = nullptr;
+            if (!arr) {   // owned-slice output: gather a full copy for the certificate (rare path)
+                CU(dmalloc(&tmp, (size_t)g->n));
+                falcon_status_t st = gather_full(g, tmp, s);
+                if (st != FALCON_OK) return st;
+                CU(cudaStreamSynchronize(s));
+                arr = tmp;
+            }
             int flag = 0;
             for (auto *p : g->parts) {
                 bool bad = false;
-                falcon_status_t st = overflow_certificate(p, p->row_off, p->col, dst, &bad);
+                falcon_status_t st = overflow_certificate(p, p->row_off, p->col, arr, &bad);
                 if (st != FALCON_OK) return st;
                 flag |= bad ? 1 : 0;
             }
+            dfree(tmp);
             if (!cm->simulated) {
-                falcon_graph *me = g->parts[0];
                 CU(cudaMemcpyAsync(me->d_flags, &flag, 4, cudaMemcpyHostToDevice, s));
                 NC(nc->AllReduce(me->d_flags, me->d_flags, 1, ncclInt32, ncclMax, cm->nccl, s));
                 CU(cudaMemcpyAsync(&flag, me->d_flags, 4, cudaMemcpyDeviceToHost, s));
@@ -742,6 +877,9 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
     dfree(d_vals);
     dfree(d_ctrls);
     for (auto *p : g->parts) p->use_unit = false;
+    g->last_mode = mode;
+    g->last_rounds = rounds;
+    g->last_host_checks = host_checks;
     if (stats) {
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, g->parts[0]->ev0, g->parts[0]->ev1));
@@ -752,7 +890,7 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
             stats->edges_relaxed += (int64_t)c.edges;
             stats->updates += (int64_t)c.updates;
         }
-        stats->kernel_launches = rounds * (algo == CC ? 3 : 4) * (int64_t)g->parts.size() + 2;
+        stats->kernel_launches = rounds * (algo == CC ? 3 : (fused ? 2 : 3)) * (int64_t)g->parts.size() + 2;
         stats->ms = ms;
         stats->relax_ms = -1.0;
     }

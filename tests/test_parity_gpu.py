@@ -154,6 +154,35 @@ def test_parity_worklist_noq(gpu_lib, name, dense_div, wl_noq, persist):
 
 
 @pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s", "ragged", "tiny"])
+@pytest.mark.parametrize("dense_div", [16, 10**6, 1])
+@pytest.mark.parametrize("dl_noq", [0, 1])
+@pytest.mark.parametrize("persist", [0, 1])
+def test_parity_delta_noq(gpu_lib, name, dense_div, dl_noq, persist):
+    """DELTA dense rounds without claims / queue (near targets marked in the
+    bitmap, far ones parked; the next round reads the bitmap, a refill round
+    builds a queue again) reach the same fixpoint for any bucket width."""
+    G = _graph(name)
+    exp = oracle.sssp(G.row_off, G.col, G.w, G.source)
+    g = _load(gpu_lib, G.n, G.row_off, G.col, G.w)
+    gpu_lib.falcon_set_option(g, "dense_div", dense_div)
+    gpu_lib.falcon_set_option(g, "dl_noq", dl_noq)
+    gpu_lib.falcon_set_option(g, "persist", persist)
+    for delta in (0, 1, 7, 10**5):
+        gpu_lib.falcon_set_delta(g, delta)
+        for local in (0, 4):
+            gpu_lib.falcon_set_option(g, "local", local)
+            for split in ((0, 2, 64) if delta == 0 else (0,)):   # bucket splits (auto Δ only)
+                gpu_lib.falcon_set_option(g, "split_div", split)
+                out, _ = _run(gpu_lib, g, "sssp", "delta", G.source)
+                assert np.array_equal(out, exp), f"{name}/dd={dense_div}/noq={dl_noq}/Δ={delta}/local={local}/split={split}"
+    gpu_lib.falcon_set_option(g, "split_div", 0)
+    exp_bfs = oracle.bfs(G.row_off, G.col, G.source)
+    gpu_lib.falcon_set_option(g, "bfs_unit", 1)   # BFS WORKLIST as unit-weight DELTA
+    out, _ = _run(gpu_lib, g, "bfs", "worklist", G.source)
+    assert np.array_equal(out, exp_bfs)
+
+
+@pytest.mark.parametrize("name", ["rand-s", "rmat-s", "grid-s", "ragged", "tiny"])
 @pytest.mark.parametrize("local", [1, 2, 16, 1000])
 @pytest.mark.parametrize("dense_div", [32, 1])
 def test_parity_local_continuation(gpu_lib, name, local, dense_div):

@@ -29,16 +29,18 @@ __global__ void __launch_bounds__(256) mix(int *win, uint32_t nwin, const uint2 
         int v[U];
         uint2 s[U];
 #pragma unroll
-        for (int g = 0; g < U; g++) {
-            const uint64_t si = (((uint64_t)i * nt + t) * U + g) % nstream;
-            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
-                : "=r"(s[g].x), "=r"(s[g].y) : "l"(stream + si), "l"(pf));
+        for (int g = 0; g < U; g++) {   // streamed 8 B per gather (nstream a power of two)
+            const uint64_t si = (((uint64_t)i * nt + t) * U + g) & (nstream - 1);
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                         : "=r"(s[g].x), "=r"(s[g].y) : "l"(stream + si), "l"(pf));
         }
 #pragma unroll
-        for (int g = 0; g < U; g++) {
-            idx[g] = hash32(t * 0x9E3779B9u + (i * U + g) * 0x85ebca6bu + salt + s[g].x) % nwin;
-            asm("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v[g]) : "l"(win + idx[g]), "l"(pl));
+        for (int g = 0; g < U; g++) {   // independent of the stream: multiply-shift into [0, nwin)
+            idx[g] = (uint32_t)(((uint64_t)hash32(t * 0x9E3779B9u + (i * U + g) * 0x85ebca6bu + salt) * nwin) >> 32);
+            asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v[g]) : "l"(win + idx[g]), "l"(pl));
         }
+#pragma unroll
+        for (int g = 0; g < U; g++) acc += (int)s[g].x;
 #pragma unroll
         for (int g = 0; g < U; g++) {
             if ((g & 7) < RED_PER8) {
@@ -81,7 +83,7 @@ int main() {
     cudaMalloc(&win, maxw); cudaMalloc(&out, 64); cudaMalloc(&stream, sbytes); cudaMalloc(&bm, maxw / 32);
     cudaMemset(win, 0x7f, maxw); cudaMemset(stream, 1, sbytes); cudaMemset(bm, 0, maxw / 32);
     const uint64_t ns = sbytes / 8;
-    for (size_t mb : {50, 100}) {
+    for (size_t mb : {24, 50, 100}) {
         const uint32_t nw = (uint32_t)((mb << 20) / 4);
         for (int occ : {4, 8}) {
             const int grid = sms * occ;

@@ -52,7 +52,7 @@ def combine(csv_path, stats_path):
     stats = json.load(open(stats_path))
     calls, cur = [], []
     for k in sorted(L):
-        nm = names[k]
+        nm = names[k].split("(")[0].replace("void ", "").replace("fk::", "").strip()
         if nm.startswith("k_finish"):
             calls.append(cur)
             cur = []
