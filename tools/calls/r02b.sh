@@ -1,5 +1,6 @@
 # GPU call: parity of the DELTA split / pull changes; sweeps
 set -x
+timeout 1500 python -m pytest tests/test_loopback_gpu.py -x -q > gpurun_out/tests_lb.log 2>&1; echo rc=$? >> gpurun_out/tests_lb.log
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -k "delta or noq or golden or tiny or star or layouts" > gpurun_out/tests_b.log 2>&1; echo rc=$? >> gpurun_out/tests_b.log
 for sd in 0 4 8 16; do
