@@ -69,6 +69,8 @@ def parse():
                     help="process-group backend for barriers / max-over-ranks (gloo: functional tests of N>1 "
                          "with several ranks sharing one GPU)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--dump", default=None, help="write every (algo, style) output this rank computed to DIR "
+                                                 "(rank<r>_<algo>_<style>.npy; tests compare them with the oracle)")
     return ap.parse_args()
 
 
@@ -353,7 +355,7 @@ def main():
     # partition mode: the same graph on every rank (each keeps its rows).
     sections = args.mode == "sections" and not partition
     if world > 1 and rank > 0 and not partition and not sections:
-        base = gg.CONFIGS[args.config]
+        base = lambda: gg.config(args.config)
         G = {"rand-25M": lambda: gg.er(25_000_000, 100_000_000, 25 + rank, name="rand-25M"),
              "rmat-10M": lambda: gg.rmat(10_000_000, 100_000_000, 10 + rank, name="rmat-10M"),
              "grid-24M": lambda: gg.grid(6000, 4000, 24 + rank, name="grid-24M")}.get(args.config, base)()
@@ -496,6 +498,15 @@ def main():
                 "t1_over_P_tP": {a: t1[a] / (P_ * tP[a]) for a in tP} if t1 and not args.simulate else None,
                 "note": "t1 = the same calls (VERTEX style) on the full graph on rank 0's GPU in this run; "
                         "exchange bytes: this rank's sends (fused: 8 B per remote improvement)"}
+
+    if args.dump:   # outputs of this rank's runs, for tests/test_sections_gpu.py
+        os.makedirs(args.dump, exist_ok=True)
+        for a, s_ in runs:
+            fb.run(g, a, s_, out, G.source)
+            np.save(os.path.join(args.dump, f"rank{rank}_{a}_{s_}.npy"), out.cpu().numpy())
+        if rank == 0:
+            json.dump({"config": args.config, "mode": args.mode, "world": world, "source": int(G.source),
+                       "runs": [list(r) for r in all_runs]}, open(os.path.join(args.dump, "meta.json"), "w"))
 
     breakdown = {}
     for (a, s), lst in per_run.items():

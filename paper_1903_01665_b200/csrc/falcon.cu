@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: one named range per C-ABI call (no link dependency)
 
 #include <cstdarg>
 #include <map>
@@ -160,6 +161,15 @@ cudaError_t dmalloc(T **p, size_t count) {
 }
 
 }  // namespace
+
+// NVTX range for the duration of one C-ABI call (visible in nsys / ncu --nvtx).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+const char *const NVTX_SSSP[4] = {"falcon_sssp VERTEX", "falcon_sssp EDGE", "falcon_sssp WORKLIST", "falcon_sssp DELTA"};
+const char *const NVTX_BFS[4] = {"falcon_bfs VERTEX", "falcon_bfs EDGE", "falcon_bfs WORKLIST", "falcon_bfs ?"};
+const char *const NVTX_CC[4] = {"falcon_cc VERTEX", "falcon_cc EDGE", "falcon_cc WORKLIST", "falcon_cc ?"};
 
 struct falcon_graph {
     int device = 0;
@@ -1217,6 +1227,7 @@ extern "C" {
 
 falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, const uint32_t *col, const int32_t *w,
                                const falcon_load_opts_t *opts, falcon_graph_t **out) {
+    NvtxRange r("graph_load_csr");
     if (!out) return fail(FALCON_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     const bool slice = opts && (opts->flags & FALCON_LOAD_SLICE);   // a rank's slice may be empty
@@ -1284,6 +1295,7 @@ falcon_status_t graph_share(falcon_graph_t *g, const falcon_load_opts_t *opts, f
 
 falcon_status_t falcon_run_many(int njobs, falcon_graph_t *const *graphs, const falcon_job_t *jobs,
                                 int32_t *const *outs, falcon_stats_t *stats) {
+    NvtxRange r("falcon_run_many");
     if (njobs < 0 || (njobs > 0 && (!graphs || !jobs || !outs))) return fail(FALCON_ERR_INVALID_ARG, "bad job arrays");
     for (int i = 0; i < njobs; i++) {
         if (!graphs[i]) return fail(FALCON_ERR_INVALID_ARG, "job %d: graph is NULL", i);
@@ -1408,20 +1420,24 @@ falcon_status_t graph_info(const falcon_graph_t *g, int64_t *n, int64_t *m) {
 
 falcon_status_t falcon_sssp(falcon_graph_t *g, uint32_t source, falcon_style_t style, int32_t *dist_out,
                             falcon_stats_t *stats) {
+    NvtxRange r(NVTX_SSSP[(unsigned)style & 3u]);
     return run(g, SSSP, source, (int)style, dist_out, stats);
 }
 
 falcon_status_t falcon_bfs(falcon_graph_t *g, uint32_t source, falcon_style_t style, int32_t *level_out,
                            falcon_stats_t *stats) {
+    NvtxRange r(NVTX_BFS[(unsigned)style & 3u]);
     return run(g, BFS, source, (int)style, level_out, stats);
 }
 
 falcon_status_t falcon_cc(falcon_graph_t *g, falcon_style_t style, int32_t *label_out, falcon_stats_t *stats) {
+    NvtxRange r(NVTX_CC[(unsigned)style & 3u]);
     return run(g, CC, 0, (int)style, label_out, stats);
 }
 
 falcon_status_t falcon_mst(falcon_graph_t *g, falcon_style_t style, int64_t *total_weight, int64_t *forest_edges,
                            int32_t *label_out, falcon_stats_t *stats) {
+    NvtxRange r("falcon_mst");
     return run_mst(g, (int)style, total_weight, forest_edges, label_out, stats);
 }
 

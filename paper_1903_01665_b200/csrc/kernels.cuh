@@ -388,16 +388,10 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
         bool found = false;
         if (v < a.n && !((visw >> lane) & 1u)) {
             nv++;
-            // in-arcs four at a time: four independent column loads, then four
-            // independent bit tests -- two dependent steps per four arcs
             const uint32_t e1 = ld_ro(a.rin_off + v + 1);
-            for (uint32_t e = ld_ro(a.rin_off + v); e < e1 && !found; e += 4) {
-                uint32_t cu[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) cu[q] = e + q < e1 ? ld_ro(a.rin_col + e + q) : NONE;
-#pragma unroll
-                for (int q = 0; q < 4; q++) found |= cu[q] != NONE && bit_test(bm_prev, cu[q]);
-                ne += e1 - e < 4 ? e1 - e : 4;
+            for (uint32_t e = ld_ro(a.rin_off + v); e < e1; e++) {
+                ne++;
+                if (bit_test(bm_prev, ld_ro(a.rin_col + e))) { found = true; break; }
             }
         }
         const unsigned mask = __ballot_sync(FULL, found);
