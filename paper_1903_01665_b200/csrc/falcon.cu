@@ -205,10 +205,12 @@ struct falcon_graph {
     int32_t bfs_unit = -1;               // BFS WORKLIST as unit-weight Δ-stepping: -1 auto (m < 3n), 0 off, 1 on
     bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
+    uint32_t pull_unv4 = 0;              // BFS VERTEX: 1 = round-1 direction rule (pull iff frontier > n / pull_div)
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     uint32_t split_div = 0;              // DELTA (auto Δ): halve the bucket when a near round hands on > n / split_div
                                          // items (FALCON_SPLIT_DIV; 0 = never)
     int32_t *val = nullptr;
+    uint8_t *lv8 = nullptr;              // BFS byte levels (kernels.cuh put_level)
     uint32_t *bm = nullptr, *fr0 = nullptr, *fr1 = nullptr;   // bm: 4 bitmaps of nwords
     uint32_t *tiles = nullptr;           // scan tile sums (load-time layout builds)
     uint32_t nwords = 0;
@@ -291,7 +293,7 @@ struct falcon_graph {
         a.wl_local_max = wl_local_max;
         a.delta_cap = delta_cap;
         a.delta_adapt = delta == 0 || unit_run ? 1u : 0u;   // auto Δ adapts per bucket; an explicit Δ is kept
-        a.val = val; a.fr0 = fr0; a.fr1 = fr1;
+        a.val = val; a.lv8 = lv8; a.fr0 = fr0; a.fr1 = fr1;
         a.bm0 = bm; a.bm1 = bm + nwords; a.bm2 = bm + 2 * (size_t)nwords; a.vis = bm + 3 * (size_t)nwords;
         a.ctrl = ctrl; a.cnt = cnt;
         return a;
@@ -410,7 +412,8 @@ struct Round {
         launches++;
         launches++;
         k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n,
-                                                 STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div);
+                                                 STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div, g->pull_unv4,
+                                                 (uint32_t)g->m);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
     }
@@ -839,6 +842,7 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
         if (trace)
             for (auto &l : lines) fprintf(stderr, "[falcon trace] %s\n", l.c_str());
     }
+    if (algo == BFS && !unit) k_bfs_levels<<<g->grid_small, BLOCK, 0, s>>>(a);   // byte levels -> val
     k_finish<<<1, BLOCK, 0, s>>>(a, (uint32_t)g->cnt_slots);
     CU(cudaGetLastError());
     CU(cudaEventRecord(g->ev1, s));
@@ -1013,7 +1017,7 @@ void destroy(falcon_graph *g) {
     if (g->ev1) cudaEventDestroy(g->ev1);
     for (void *p : {(void *)g->row_off, (void *)g->col, (void *)g->w, (void *)g->cw, (void *)g->src,
                     (void *)g->rin_off, (void *)g->rin_col, (void *)g->rowb, (void *)g->cwb, (void *)g->srcb,
-                    (void *)g->chunk, (void *)g->chunkb, (void *)g->chunks, (void *)g->val, (void *)g->bm,
+                    (void *)g->chunk, (void *)g->chunkb, (void *)g->chunks, (void *)g->val, (void *)g->lv8, (void *)g->bm,
                     (void *)g->fr0, (void *)g->fr1, (void *)g->tiles, (void *)g->ctrl, (void *)g->cnt,
                     (void *)g->d_flags, (void *)g->mst_best, (void *)g->mst_list, (void *)g->xcounts,
                     (void *)g->xcnt_recv, (void *)g->outbox, (void *)g->inbox, (void *)g->bounds_d,
@@ -1048,12 +1052,14 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     CU(dmalloc(&g->col, (size_t)m));
     CU(dmalloc(&g->w, (size_t)m));
     CU(dmalloc(&g->val, (size_t)n));
+    CU(dmalloc(&g->lv8, ((size_t)n + 15) / 16 * 16 + 16));
     g->nwords = (uint32_t)((((n + 31) / 32) + 3) & ~3ll);
     CU(dmalloc(&g->bm, 4 * (size_t)g->nwords));
     CU(dmalloc(&g->fr0, (size_t)n + 1));
     CU(dmalloc(&g->fr1, (size_t)n + 1));   // n+1: doubles as the reverse-CSR cursor at build time
     CU(dmalloc(&g->tiles, (size_t)(MAX_BLK * ((uint64_t)n + 1) + 1023) / 1024 + 1));   // scan tile sums
     CU(dmalloc(&g->ctrl, 1));
+    CU(cudaMemsetAsync(g->ctrl, 0, sizeof(Ctrl), s));   // padding / unused fields: the whole block is copied out
     CU(dmalloc(&g->d_flags, 1));
     CU(host_ctrl_alloc(reinterpret_cast<void **>(&g->h_ctrl), sizeof(Ctrl)));
 
@@ -1111,6 +1117,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (const char *bd = getenv("FALCON_BLOCK_DIV")) g->blk_div = (uint32_t)atoi(bd);          // 0: never blocked
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
+    if (const char *pu = getenv("FALCON_BFS_PULL_UNV")) g->pull_unv4 = (uint32_t)atoi(pu);
     int slots = g->grid_persist;
     for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_edge_b, g->grid_small, g->grid_cc,
                     g->grid_pull})
@@ -1187,7 +1194,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->dl_noq = p->dl_noq; v->split_div = p->split_div; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
     v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
-    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div;
+    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_unv4 = p->pull_unv4;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
     v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
     v->grid_pull = p->grid_pull; v->grid_cc = p->grid_cc; v->grid_edge = p->grid_edge; v->grid_edge_b = p->grid_edge_b;
@@ -1206,10 +1213,12 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     CU(cudaEventCreate(&v->ev1));
     const size_t n = (size_t)p->n;
     CU(dmalloc(&v->val, n));
+    CU(dmalloc(&v->lv8, (n + 15) / 16 * 16 + 16));
     CU(dmalloc(&v->bm, 4 * (size_t)v->nwords));
     CU(dmalloc(&v->fr0, n + 1));
     CU(dmalloc(&v->fr1, n + 1));
     CU(dmalloc(&v->ctrl, 1));
+    CU(cudaMemsetAsync(v->ctrl, 0, sizeof(Ctrl), v->stream));
     CU(dmalloc(&v->cnt, 3 * (size_t)v->cnt_slots));
     CU(dmalloc(&v->d_flags, 1));   // the view's own (overflow certificate)
     CU(host_ctrl_alloc(reinterpret_cast<void **>(&v->h_ctrl), sizeof(Ctrl)));
@@ -1488,6 +1497,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->wl_local_max = (uint32_t)std::min<int64_t>(value, 0xffffffffll);
         } else if (!strcmp(name, "pull_div")) {
             t->pull_div = (uint32_t)value;
+        } else if (!strcmp(name, "pull_unv")) {
+            t->pull_unv4 = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {
             if (value && t->grid_persist <= 0) return fail(FALCON_ERR_UNSUPPORTED, "cooperative launch unavailable");
             t->persist = value != 0;

@@ -58,6 +58,8 @@ struct Ctrl {
     uint32_t source;
     uint32_t pull;        // BFS VERTEX: this round runs bottom-up (pull over in-arcs)
     uint32_t found;       // BFS: vertices discovered this round (direction heuristic)
+    uint32_t visited;     // BFS: vertices discovered so far (direction heuristic)
+    unsigned long long rnd_items, rnd_edges;   // BFS VERTEX: items expanded / arcs scanned this round
     uint32_t thr;         // DELTA: current bucket threshold T (near: dist < T)
     uint32_t delta;       // DELTA: bucket width
     uint32_t minpend;     // DELTA: min tentative distance parked in the far set
@@ -118,6 +120,7 @@ struct Args {
     const uint32_t *rin_off;   // [n+1] reverse CSR (in-arcs), BFS pull only
     const uint32_t *rin_col;   // [m]
     int32_t *val;              // dist / level / label [n]
+    uint8_t *lv8;              // BFS: levels < 255 as bytes [n] (0xFF: none), merged into val by k_bfs_levels
     uint32_t *bm0, *bm1, *bm2; // round bitmaps [nwords] each
     uint32_t *vis;             // BFS visited bitmap [nwords]
     uint32_t *fr0, *fr1;       // frontier queues [n] each
@@ -195,6 +198,17 @@ __device__ __forceinline__ uint32_t ld_ro(const uint32_t *p) { return __ldg(p); 
 
 __device__ __forceinline__ bool bit_test(const uint32_t *bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
 
+// BFS level L of vertex v (PAPER.md:1309 `t.dist = lev+1`).  Levels below 255
+// go to a byte array (n bytes: L2-resident at 25M vertices, where the int32
+// array is 100 MB): each round's scattered level stores would otherwise
+// partially dirty most sectors of the 100 MB value array and cost a DRAM
+// read-modify-write of all of it (ncu: ~200 MB per pull round on rand-25M).
+// Deeper levels are stored in val directly; k_bfs_levels merges at the end.
+__device__ __forceinline__ void put_level(const Args &a, uint32_t v, uint32_t L) {
+    if (L < 255u) a.lv8[v] = (uint8_t)L;
+    else a.val[v] = (int32_t)L;
+}
+
 // ------------------------------------------------------------------ block primitives
 template <int B>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t &total, uint32_t *s_warp) {
@@ -236,10 +250,12 @@ __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long
         ne += __shfl_down_sync(FULL, ne, o);
         nu += __shfl_down_sync(FULL, nu, o);
     }
+    __syncwarp();      // bar.sync is .aligned: the warp must arrive converged (compute-sanitizer synccheck)
     __syncthreads();
     if (lane == 0) { s_red[0][wid] = nv; s_red[1][wid] = ne; s_red[2][wid] = nu; }
     if (chg) atomicOr(&s_flags, 1);
     if (ovf) atomicOr(&s_flags, 2);
+    __syncwarp();
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long t0 = 0, t1 = 0, t2 = 0;
@@ -247,6 +263,8 @@ __device__ __forceinline__ void flush_counters(const Args &a, unsigned long long
         unsigned long long *c = a.cnt + 3ull * blockIdx.x;   // this CTA's private slot: no atomics
         c[0] += t0; c[1] += t1; c[2] += t2;
         if (t2) atomicAdd(&a.ctrl->found, (uint32_t)(t2 < 0xffffffffull ? t2 : 0xffffffffull));   // density heuristics
+        if (t0) atomicAdd(&a.ctrl->rnd_items, t0);   // direction heuristic (BFS VERTEX)
+        if (t1) atomicAdd(&a.ctrl->rnd_edges, t1);
         if (s_flags & 1) a.ctrl->changed = 1;
         if (s_flags & 2) a.ctrl->cand_ovf = 1;   // not an error by itself (R3): checked after the fixpoint
     }
@@ -268,9 +286,27 @@ template <int ALGO>
 __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, int style, uint32_t delta) {
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
-    for (uint32_t v = t0; v < a.n; v += stride) {
-        if (ALGO == CC) a.val[v] = (int32_t)v;
-        else a.val[v] = v == source ? 0 : INF;
+    if (ALGO == BFS) {   // levels start in the byte array (0xFF: none); val is written by k_bfs_levels
+        uint4 *l4 = reinterpret_cast<uint4 *>(a.lv8);
+        const uint32_t n16 = (a.n + 15) / 16;
+        for (uint32_t i = t0; i < n16; i += stride) {
+            uint4 x = make_uint4(~0u, ~0u, ~0u, ~0u);
+            if (i == source / 16) {   // the source is at level 0
+                const uint32_t keep = ~(0xFFu << (8 * (source % 4)));
+                switch ((source % 16) / 4) {
+                case 0: x.x &= keep; break;
+                case 1: x.y &= keep; break;
+                case 2: x.z &= keep; break;
+                default: x.w &= keep; break;
+                }
+            }
+            l4[i] = x;
+        }
+    } else {
+        for (uint32_t v = t0; v < a.n; v += stride) {
+            if (ALGO == CC) a.val[v] = (int32_t)v;
+            else a.val[v] = v == source ? 0 : INF;
+        }
     }
     const uint32_t sw = ALGO == CC ? 0xffffffffu : source >> 5, sb = 1u << (source & 31);
     for (uint32_t i = t0; i < a.nwords; i += stride) {
@@ -288,13 +324,45 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->all_active = ALGO == CC ? 1u : 0u;
         c->status = ST_OK; c->source = source;
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
-        c->pull = 0; c->found = 0;
+        c->pull = 0; c->found = 0; c->visited = 1; c->rnd_items = 0; c->rnd_edges = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
         c->delta0 = delta; c->delta_adapt = a.delta_adapt; c->bk_rounds = 0; c->bk_items = 0;
         c->delta_cap = a.delta_cap ? a.delta_cap : 128u;
         c->bar_arrive = 0; c->blk = 0; c->noq = 0; c->prevnoq = 0; c->hooks = 0; c->wsum = 0; c->cand_ovf = 0;
         c->xremote = 0;
         if (ALGO != CC) a.fr0[0] = source;
+    }
+}
+
+// BFS epilogue: val[v] = byte level if v got one, INF if v was never
+// discovered; a vertex discovered at level >= 255 already has its level in
+// val (put_level).  Four vertices per thread, a full 16-byte store when none
+// of the four keeps its value -- val is never read for a shallow BFS.
+__global__ void k_bfs_levels(Args a) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t n4 = (a.n + 3) / 4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint32_t b4 = reinterpret_cast<const uint32_t *>(a.lv8)[i];
+        const uint32_t vw = (a.vis[i >> 3] >> ((i & 7) * 4)) & 0xFu;   // visited bits of vertices 4i .. 4i+3
+        int32_t o[4];
+        bool keep = false;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t b = (b4 >> (8 * j)) & 0xFFu;
+            const bool visited = (vw >> j) & 1u;
+            o[j] = b != 0xFFu ? (int32_t)b : INF;
+            if (b == 0xFFu && visited) keep = true;   // level >= 255, in val already
+        }
+        if (!keep && 4 * i + 4 <= a.n) {
+            reinterpret_cast<int4 *>(a.val)[i] = make_int4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t v = 4 * i + j;
+                const bool visited = (vw >> j) & 1u;
+                if (v < a.n && !(((b4 >> (8 * j)) & 0xFFu) == 0xFFu && visited)) a.val[v] = o[j];
+            }
+        }
     }
 }
 
@@ -366,9 +434,23 @@ __global__ void k_sum_weights(uint64_t m, const int32_t *w, unsigned long long *
 // ------------------------------------------------------------------ BFS bottom-up (pull) round
 // Direction-optimising BFS, VERTEX style over `innbrs` (Table
 // "Iterators"): every unvisited vertex scans its in-arcs until it finds a
-// parent in the previous level (bm[(r-1)%3]).  A warp owns one 32-vertex
-// bitmap word, so the visited / next-frontier words are written with plain
-// stores.  Run when the frontier is large (k_advance).
+// parent in the previous level (bm[(r-1)%3]).  Run when the frontier is large
+// (k_advance).
+//
+// Two forms, chosen per round by bfs_direction (Ctrl::pull):
+//  1 = word: a warp owns one bitmap word at a time, lane i scans the in-arcs
+//      of vertex 32w + i if it is unvisited -- for a large unvisited set,
+//      where most lanes have work;
+//  2 = compacted: a warp owns groups of PG = 16 words (512 vertices, one word
+//      per lane); the group's UNVISITED vertices are compacted into a
+//      shared-memory list and walked two per lane, so every lane carries two
+//      independent early-exit scans (rin_col load -> parent bit test) however
+//      few vertices of a word are still unvisited (the word form left most
+//      lanes idle when 6 % of the vertices were unvisited: rand-25M 150 us
+//      -> 95 us for that round, but 309 -> 370 us on a round with 72 %).
+//      Parents found are collected in a per-warp shared word array, so the
+//      visited / next-frontier words are written once, with plain stores, by
+//      the lane owning the word.
 template <int B>
 __global__ void __launch_bounds__(B) k_pull(Args a) {
     Ctrl *c = a.ctrl;
@@ -377,29 +459,102 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
     clear_next_bitmap(a, iter);
     const uint32_t *bm_prev = bm_of(a, iter - 1);
     uint32_t *bm_now = bm_of(a, iter);
-    const int lane = threadIdx.x & 31;
+    if (c->pull == 1) {
+        const int lane = threadIdx.x & 31;
+        const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
+        unsigned long long nv = 0, ne = 0, nu = 0;
+        bool chg = false;
+        for (uint32_t wi = gw; wi < a.nwords; wi += nwarps) {
+            const uint32_t visw = a.vis[wi];
+            const uint32_t v = wi * 32u + lane;
+            if ((bm_prev[wi] >> lane) & 1u) put_level(a, v, lev);   // discovered last round
+            bool found = false;
+            if (v < a.n && !((visw >> lane) & 1u)) {
+                nv++;
+                const uint32_t e1 = ld_ro(a.rin_off + v + 1);
+                for (uint32_t e = ld_ro(a.rin_off + v); e < e1; e++) {
+                    ne++;
+                    if (bit_test(bm_prev, ld_ro(a.rin_col + e))) { found = true; break; }
+                }
+            }
+            const unsigned mask = __ballot_sync(FULL, found);
+            if (mask && lane == 0) {
+                a.vis[wi] = visw | mask;
+                bm_now[wi] = mask;
+            }
+            if (found) { nu++; chg = true; }
+        }
+        flush_counters<B>(a, nv, ne, nu, chg, false);
+        return;
+    }
+    // 16-word groups: 16.5 KB of shared memory per CTA keeps 8 CTAs of 256
+    // threads resident per SM (one wave), and a round has enough groups per
+    // warp to balance (32-word groups: 6 CTAs/SM, two waves, 2x slower)
+    constexpr uint32_t PG = 16;
+    __shared__ uint32_t s_it[B / 32][PG * 32];
+    __shared__ uint32_t s_fd[B / 32][PG];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *sit = s_it[wid], *sfd = s_fd[wid];
     const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
     unsigned long long nv = 0, ne = 0, nu = 0;
     bool chg = false;
-    for (uint32_t wi = gw; wi < a.nwords; wi += nwarps) {
-        const uint32_t visw = a.vis[wi];
-        const uint32_t v = wi * 32u + lane;
-        if ((bm_prev[wi] >> lane) & 1u) a.val[v] = (int32_t)lev;   // discovered last round
-        bool found = false;
-        if (v < a.n && !((visw >> lane) & 1u)) {
-            nv++;
-            const uint32_t e1 = ld_ro(a.rin_off + v + 1);
-            for (uint32_t e = ld_ro(a.rin_off + v); e < e1; e++) {
-                ne++;
-                if (bit_test(bm_prev, ld_ro(a.rin_col + e))) { found = true; break; }
+    for (uint32_t g0 = gw * PG; g0 < a.nwords; g0 += nwarps * PG) {   // warp-uniform
+        const uint32_t wi = g0 + lane;
+        uint32_t visw = 0xffffffffu, prevw = 0;
+        if (lane < PG && wi < a.nwords) { visw = a.vis[wi]; prevw = bm_prev[wi]; }
+        // the level of the vertices discovered last round: one coalesced
+        // 128-byte store per non-empty word
+        for (unsigned pm = __ballot_sync(FULL, prevw != 0); pm; pm &= pm - 1) {   // warp-uniform
+            const int j = __ffs(pm) - 1;
+            if ((__shfl_sync(FULL, prevw, j) >> lane) & 1u) put_level(a, (g0 + j) * 32u + lane, lev);
+        }
+        uint32_t unv = ~visw;
+        const uint64_t v0w = (uint64_t)wi * 32u;   // vertices >= n count as visited
+        if (v0w >= a.n) unv = 0;
+        else if (v0w + 32 > a.n) unv &= (1u << (uint32_t)(a.n - v0w)) - 1u;
+        const uint32_t cnt = __popc(unv);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        if (total == 0) continue;
+        uint32_t pos = incl - cnt;
+        for (uint32_t y = unv; y; y &= y - 1) sit[pos++] = wi * 32u + (uint32_t)(__ffs(y) - 1);
+        if (lane < PG) sfd[lane] = 0u;
+        __syncwarp();
+        nv += cnt;
+        for (uint32_t j0 = 0; j0 < total; j0 += 64) {   // warp-uniform
+            const uint32_t va = j0 + lane < total ? sit[j0 + lane] : NONE;
+            const uint32_t vb = j0 + 32 + lane < total ? sit[j0 + 32 + lane] : NONE;
+            uint32_t ea = 0, eae = 0, eb = 0, ebe = 0;
+            if (va != NONE) { ea = ld_ro(a.rin_off + va); eae = ld_ro(a.rin_off + va + 1); }
+            if (vb != NONE) { eb = ld_ro(a.rin_off + vb); ebe = ld_ro(a.rin_off + vb + 1); }
+            bool fa = false, fb = false;
+            while (ea < eae || eb < ebe) {   // two independent early-exit scans per lane
+                const bool la = ea < eae, lb = eb < ebe;
+                const uint32_t sa = la ? ld_ro(a.rin_col + ea) : 0u;
+                const uint32_t sb = lb ? ld_ro(a.rin_col + eb) : 0u;
+                const bool ha = la && bit_test(bm_prev, sa);
+                const bool hb = lb && bit_test(bm_prev, sb);
+                ne += (uint32_t)la + (uint32_t)lb;
+                if (ha) { fa = true; ea = eae; } else ea += la;
+                if (hb) { fb = true; eb = ebe; } else eb += lb;
             }
+            if (fa) atomicOr(sfd + ((va >> 5) - g0), 1u << (va & 31));
+            if (fb) atomicOr(sfd + ((vb >> 5) - g0), 1u << (vb & 31));
         }
-        const unsigned mask = __ballot_sync(FULL, found);
-        if (mask && lane == 0) {
-            a.vis[wi] = visw | mask;
-            bm_now[wi] = mask;
+        __syncwarp();
+        const uint32_t nw = lane < PG ? sfd[lane] : 0u;
+        if (nw) {
+            a.vis[wi] = visw | nw;
+            bm_now[wi] = nw;
+            nu += __popc(nw);
+            chg = true;
         }
-        if (found) { nu++; chg = true; }
+        __syncwarp();
     }
     flush_counters<B>(a, nv, ne, nu, chg, false);
 }
@@ -611,7 +766,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
                 } else {   // VERTEX: the level is written when the vertex is expanded next round
                     atomicOr(a.vis + (s.v[q] >> 5), 1u << (s.v[q] & 31));
                     atomicOr(x.bm_now + (s.v[q] >> 5), 1u << (s.v[q] & 31));
-                    if (NOQ) a.val[s.v[q]] = (int32_t)(x.lev + 1);
+                    if (NOQ) put_level(a, s.v[q], x.lev + 1);
                     acc.nu++; acc.chg = true;
                 }
             }
@@ -663,7 +818,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
         for (int q = 0; q < U; q++) {
             const bool want = need[q] && !(got[q] & (1u << (citem[q] & 31)));
             if (ALGO == BFS && want) {
-                a.val[citem[q]] = (int32_t)(x.lev + 1);
+                put_level(a, citem[q], x.lev + 1);
                 atomicOr(x.bm_now + (citem[q] >> 5), 1u << (citem[q] & 31));   // dense rounds read it
                 acc.nu++; acc.chg = true;
             }
@@ -808,7 +963,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                     item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
                     if (u != NONE && first) {
                         acc.nv++;
-                        if (ALGO == BFS && is_vertex(STYLE)) a.val[u] = (int32_t)x.lev;   // discovered last round
+                        if (ALGO == BFS && is_vertex(STYLE)) put_level(a, u, x.lev);   // discovered last round
                     }
                     if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
                     if (STYLE == DELTA && u != NONE && pay >= x.thr) {   // bucket was split: back to the far set
@@ -1006,7 +1161,7 @@ __device__ __forceinline__ void edge_quad(const Args &a, uint32_t q, const uint3
         } else if (ALGO == BFS) {   // e.src.dist == lev (R14) via the bitmap
             if (cur[j] == INF) {
                 atomicOr(a.vis + (d[j] >> 5), 1u << (d[j] & 31));
-                a.val[d[j]] = (int32_t)(lev + 1);
+                put_level(a, d[j], lev + 1);
                 atomicOr(bm_now + (d[j] >> 5), 1u << (d[j] & 31));
                 nu++; chg = true;
             }
@@ -1160,13 +1315,42 @@ __global__ void k_compress(Args a) {
 }
 
 // ------------------------------------------------------------------ round advance
+// Direction of the next BFS VERTEX round (direction-optimising BFS): 0 push
+// (top-down over the frontier's out-arcs), 1 / 2 pull (bottom-up over the
+// unvisited vertices' in-arcs; 2 = the compacted form for a sparse unvisited
+// set).  Estimated L2 requests of each (random 32-byte sectors; the measured
+// cost unit of every relax kernel here), from F = the new
+// frontier, U = unvisited vertices, d = arcs per item of this push round (or
+// m/n after a pull round) and m_f = F d:
+//   push ~ m_f (a visited-bit gather per arc) + 2F (row offsets and arcs of
+//          each frontier vertex) + 2.5 x expected discoveries
+//          U (1 - exp(-m_f / n)) (visited and frontier REDs, level store),
+//   pull ~ 2U (in-arc offsets and first in-arcs of each unvisited vertex)
+//          + U min(m/n, m/m_f) (in-arcs scanned until a parent: 1/p with
+//          p = m_f/m the frontier's share of the in-arcs).
+// pull_div keeps the round-1 rule instead (pull iff F > n / pull_div) when
+// unv4 is set to 1 (FALCON_BFS_PULL_UNV=1).  Only the schedule changes.
+__device__ __forceinline__ uint32_t bfs_direction(const Ctrl *c, uint32_t n, uint64_t m, uint32_t pull_div,
+                                                  uint32_t unv4) {
+    if (!pull_div || c->found == 0) return 0;
+    if (unv4 == 1) return c->found > n / pull_div ? 1u : 0u;
+    const float F = (float)c->found, U = (float)(n - c->visited), N = (float)n, M = (float)m;
+    if (c->found <= n / 1024u) return 0;   // small frontier: push
+    const float d = !c->pull && c->rnd_items ? (float)c->rnd_edges / (float)c->rnd_items : M / N;
+    const float mf = F * d;
+    const float push = mf + 2.f * F + 2.5f * U * (1.f - __expf(-mf / N));
+    const float pull = 2.f * U + U * fminf(M / N, mf > 0.f ? M / mf : M / N);
+    if (pull >= push) return 0;
+    return U * 2.f < N ? 2u : 1u;
+}
+
 // Decides on the device whether another round runs ("if
 // (changed == 0) break" / SPEC.md:221 "worklist non-empty"), and drives the
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 // aux_div: BFS VERTEX: pull_div (bottom-up threshold); DELTA: split_div (bucket split)
 template <int ALGO, int STYLE>
 __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t aux_div,
-                                             uint32_t blk_div) {
+                                             uint32_t blk_div, uint32_t unv4 = 0, uint64_t m = 0) {
     const uint32_t pull_div = aux_div;
     if (c->done) return false;
     c->launches += launches_per_round;
@@ -1237,7 +1421,12 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
         } else if (STYLE == VERTEX) {
             c->in_len = 0;   // VERTEX rounds read the activity bitmap
             // direction-optimising BFS: bottom-up while the next frontier is large
-            if (ALGO == BFS) c->pull = pull_div && c->found > n / pull_div;
+            if (ALGO == BFS) {
+                c->visited += c->found;
+                c->pull = bfs_direction(c, n, m, pull_div, unv4);
+                c->rnd_items = 0;
+                c->rnd_edges = 0;
+            }
             // SSSP: the next round walks the destination-blocked layout when this
             // round improved many vertices (its frontier is large)
             c->blk = blk_div && c->found > n / blk_div;
@@ -1254,9 +1443,9 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
 __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
-                          uint32_t n, uint32_t pull_div, uint32_t blk_div) {
+                          uint32_t n, uint32_t pull_div, uint32_t blk_div, uint32_t unv4, uint32_t m) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div);
+    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div, unv4, m);
     if (in_graph) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 

@@ -70,9 +70,10 @@ def test_sparse_exchange_moves_fewer_bytes(gpu_lib):
         moved[ex] = fb.graph_exchange_bytes(g)
     assert 0 < moved[2] < moved[1] / 10
     assert moved[0] == moved[1]   # simulated parts: auto keeps the dense device reduce
-    fb.falcon_set_option(g, "exchange", 3)   # fused: no exchange step at all
+    fb.falcon_set_option(g, "exchange", 3)   # fused: no exchange step; the remote REDs (8 B each) are counted
     fb.run(g, "sssp", "vertex", out, G.source)
-    assert np.array_equal(out, oracle.run("sssp", G)) and fb.graph_exchange_bytes(g) == 0
+    assert np.array_equal(out, oracle.run("sssp", G))
+    assert 0 < fb.graph_exchange_bytes(g) < moved[1]
 
 
 def test_simulated_partition_device_output_and_repeat(gpu_lib):
