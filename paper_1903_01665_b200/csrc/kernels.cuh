@@ -105,6 +105,7 @@ struct Args {
     uint32_t blk_div;          // ... and walks the blocked layout when it exceeds n / blk_div (0: never)
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
     uint32_t dl_noq;           // ... DELTA dense rounds (near marks in the bitmap, far parking as usual)
+    uint32_t cta_thr;          // rows longer than this are expanded by the whole CTA (0: warp-level only)
     // fused partitioned rounds (VFUSED): owned range, part bounds and the
     // owners' value arrays / round bitmaps (peer memory on real GPUs)
     uint32_t lo, hi, nparts;
@@ -621,7 +622,12 @@ struct Xw {
     Ctrl *c;
     uint32_t lev, thr, qh, qn, pend_min;   // wq[qh, qn): staged appends / the local stack (LOCAL)
     uint64_t pf, pl;
+    // CTA-level expansion: rows longer than hthr arcs are handed to the CTA
+    // (shared list hb/hd/hp of HMAX rows, count *hn; hthr = 0: off)
+    uint32_t *hb, *hd, *hp, *hn;
+    uint32_t hthr;
 };
+constexpr uint32_t HMAX = 64;   // long rows per CTA and round (more: the warp expands them itself)
 
 // Local continuation (LOCAL rounds): hand the warp's unexpanded local items
 // wq[qh, qn) over to the next round -- claim each in this round's bitmap and
@@ -857,6 +863,10 @@ template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ, bool LOCAL = fals
 __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, uint32_t deg, uint32_t pay,
                                            RoundAcc &acc, Step<U> &pend) {
     const int lane = threadIdx.x & 31;
+    if (!COHERENT && x.hthr && deg > x.hthr) {   // a long row: expanded by the whole CTA (cta_heavy)
+        const uint32_t slot = atomicAdd(x.hn, 1u);
+        if (slot < HMAX) { x.hb[slot] = beg; x.hd[slot] = deg; x.hp[slot] = pay; deg = 0; }
+    }
     uint32_t incl = deg;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -901,12 +911,58 @@ __device__ __forceinline__ void relax_tile(const Args &a, Xw &x, uint32_t beg, u
     }
 }
 
+// CTA-level cooperative expansion (north_star item 3; the load imbalance of
+// skewed degrees): the rows longer than x.hthr arcs that
+// this CTA's warps met in the round were listed in shared memory
+// (relax_tile); after every warp's own work all warps of the CTA walk them
+// together, each row 32*U arcs per warp step, warps interleaved -- an RMAT
+// hub or a star centre costs a CTA deg / (32 U W) steps instead of one warp
+// deg / (32 U).  All arcs of a step belong to one row, so no search is
+// needed.  Every thread of the CTA must call this (block barriers).
+template <int ALGO, int STYLE, int U, bool NOQ, bool LOCAL>
+__device__ __forceinline__ void cta_heavy(const Args &a, Xw &x, RoundAcc &acc) {
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t nh = min(*x.hn, HMAX);
+    Step<U> pend;
+    pend.live = false;
+    for (uint32_t h = 0; h < nh; h++) {
+        const uint32_t beg = x.hb[h], deg = x.hd[h], pay = x.hp[h];
+        if (threadIdx.x == 0) acc.ne += deg;
+        for (uint32_t base = (uint32_t)wid * 32u * U; base < deg; base += (uint32_t)nw * 32u * U) {   // warp-uniform
+            Step<U> nx;
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                const uint32_t k = base + (uint32_t)q * 32u + lane;
+                nx.ok[q] = k < deg;
+                nx.p[q] = pay;
+                nx.v[q] = 0; nx.wt[q] = 0;
+                if (nx.ok[q]) {
+                    if (ALGO == SSSP) {
+                        const uint2 w2 = ld_stream2(x.arcs + beg + k, x.pf);
+                        nx.v[q] = w2.x; nx.wt[q] = (int32_t)w2.y;
+                    } else {
+                        nx.v[q] = ld_stream(a.col + beg + k, x.pf);
+                    }
+                }
+            }
+            if (pend.live) relax_step<ALGO, STYLE, U, false, NOQ, LOCAL>(a, x, pend, acc);
+            pend = nx;
+            pend.live = true;
+        }
+    }
+    if (pend.live) relax_step<ALGO, STYLE, U, false, NOQ, LOCAL>(a, x, pend, acc);
+    __syncthreads();
+    if (threadIdx.x == 0) *x.hn = 0;
+}
+
 // One round of expansion by this warp.  sit: the warp's 1024-entry shared
 // item list (dense rounds).
 template <int ALGO, int STYLE, int U, bool COHERENT, bool NOQ = false, bool LOCAL = false>
 __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t iter, uint32_t thr, const uint32_t *in,
                                              uint32_t *out, uint32_t nitems, bool dense, bool blocked, uint32_t *wq,
-                                             uint32_t *sit, RoundAcc &acc, uint32_t ltiles = 0) {
+                                             uint32_t *sit, RoundAcc &acc, uint32_t ltiles = 0,
+                                             uint32_t *heavy = nullptr) {
     constexpr bool QUEUE = STYLE == WORKLIST || STYLE == DELTA;
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -915,6 +971,8 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
     x.bm_now = bm_of(a, iter); x.bm_prev = bm_of(a, iter - 1); x.out = out; x.wq = wq; x.c = c;
     x.lev = iter - 1; x.thr = thr; x.qh = 0; x.qn = 0; x.pend_min = 0xffffffffu;
     x.pf = pol_evict_first(); x.pl = pol_evict_last();
+    x.hthr = heavy && !COHERENT ? a.cta_thr : 0u;   // heavy: the CTA's shared long-row list
+    if (x.hthr) { x.hn = heavy; x.hb = heavy + 1; x.hd = heavy + 1 + HMAX; x.hp = heavy + 1 + 2 * HMAX; }
     blocked = blocked && ALGO == SSSP && a.nblk > 1;
     const uint32_t K = blocked ? a.nblk : 1u;
     Step<U> pend;
@@ -1000,6 +1058,9 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
         }
     }
     if (pend.live) relax_step<ALGO, STYLE, U, COHERENT, NOQ, LOCAL>(a, x, pend, acc);   // drain the pipeline
+    if constexpr (!COHERENT) {
+        if (x.hthr) cta_heavy<ALGO, STYLE, U, NOQ, LOCAL>(a, x, acc);   // before the local continuation: its stacks
+    }
     if constexpr (LOCAL) {
         // Local continuation: the warp expands the targets it improved itself,
         // 32 at a time, up to ltiles tiles, instead of leaving each hop to
@@ -1080,6 +1141,9 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     const bool blocked = is_vertex(STYLE) ? c->blk != 0 : (a.blk_div && nitems > a.n / a.blk_div);
     __shared__ uint32_t s_q[B / 32][WQ];
     __shared__ uint32_t s_it[B / 32][1024];
+    __shared__ uint32_t s_heavy[1 + 3 * HMAX];   // count, then beg / deg / pay of the CTA's long rows
+    if (threadIdx.x == 0) s_heavy[0] = 0u;
+    __syncthreads();
     RoundAcc acc;
     if ((STYLE == WORKLIST && dense && a.wl_noq) || (STYLE == DELTA && dense && a.dl_noq)) {
         // dense WORKLIST / DELTA round: items from the bitmap, improved vertices
@@ -1089,18 +1153,18 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         // sparse, it builds the queue again with claims.
         if (blockIdx.x == 0 && threadIdx.x == 0) c->noq = 1;
         expand_round<ALGO, STYLE, U, false, true>(a, c, iter, thr, in, out, nitems, true, blocked,
-                                                  s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
+                                                  s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc, 0, s_heavy);
     } else if (ALGO == SSSP && (STYLE == DELTA ? a.local_tiles && nitems <= a.local_max && !c->prevnoq
                                                : a.wl_local_tiles && nitems <= a.wl_local_max && !c->prevnoq) &&
                !dense && !blocked) {
         // sparse SSSP rounds with local continuation (expand_round)
         expand_round<ALGO, STYLE, U, false, false, ALGO == SSSP>(
             a, c, iter, thr, in, out, nitems, false, false, s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc,
-            STYLE == DELTA ? a.local_tiles : a.wl_local_tiles);
+            STYLE == DELTA ? a.local_tiles : a.wl_local_tiles, s_heavy);
     } else {
         expand_round<ALGO, STYLE, U, false>(a, c, iter, thr, in, out, nitems,
                                             dense || ((STYLE == WORKLIST || STYLE == DELTA) && c->prevnoq), blocked,
-                                            s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc);
+                                            s_q[threadIdx.x >> 5], s_it[threadIdx.x >> 5], acc, 0, s_heavy);
     }
     if (STYLE == VFUSED) __threadfence_system();   // remote REDs performed before the termination collective
     flush_counters<B>(a, acc.nv, acc.ne, acc.nu, acc.chg, acc.ovf);
