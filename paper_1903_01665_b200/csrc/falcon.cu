@@ -368,8 +368,14 @@ void launch_expand_warp(const falcon_graph *g, cudaStream_t s, const Args &a) {
     case 3: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 6>, g->grid_expand_fr, s, a); break;
     case 4: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 2>, g->grid_expand_fr, s, a); break;
     default:   // tuned per style (tools/survey.py sweeps on rand-25M / rmat-10M)
-        if (STYLE == DELTA) launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 4>, g->grid_expand_dl, s, a);
-        else launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 3>, g->grid_expand_fr, s, a);
+        // DELTA: U = 4 / 3 CTAs per SM where rounds are heavy (rand-25M 3.38 -> 3.08 ms,
+        // rmat-10M 4.39 -> 3.14 ms against U = 2 / 4 CTAs), U = 2 / 4 CTAs on sparse
+        // high-diameter graphs, whose small local-continuation rounds want the warps
+        // (grid-24M 41 ms against 66 ms with U = 4)
+        if (STYLE == DELTA && g->m < 3 * g->n)
+            launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 4>, g->grid_expand_dl, s, a);
+        else
+            launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 3>, g->grid_expand_fr, s, a);
         break;
     }
 }
