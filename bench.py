@@ -145,7 +145,14 @@ def relax_roofline(cfg, algo, style, st, G, hbm, hbm_src, traffic, traffic_src):
     if t:
         r["dram_over_algorithmic"] = t["dram_over_alg"]
         r["lts_throughput_pct"] = t["lts_throughput_pct_time_weighted"]
-        r["traffic_source"] = traffic_src
+        r["traffic_source"] = traffic_src + " (ncu default cache control: L2 flushed before every launch)"
+        for k in ("lts_sectors_per_relaxed_arc", "lts_sectors_atom", "lts_sectors_red", "lts_hit_pct_time_weighted"):
+            if k in t:
+                r[k] = t[k]
+        if "warm" in t:   # the same launches with L2 kept across launches (ncu --cache-control none)
+            w = t["warm"]
+            r["traffic_warm"] = w["dram_bytes"] / max(1, w["relax_launches"])
+            r["dram_over_algorithmic_warm"] = w["dram_over_alg"]
     try:   # secondary ceiling: random L2 operations
         pk = json.load(open(os.path.join(ROOT, "profiles", "l2_peaks.json")))
         ops = l2_ops(algo, style, st)
@@ -243,9 +250,19 @@ def traffic_table():
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
         try:
-            return json.load(open(p))["calls"], os.path.relpath(p, ROOT)
+            calls = json.load(open(p))["calls"]
         except (OSError, KeyError, ValueError):
             continue
+        # the same calls measured warm (ncu --cache-control none: L2 kept
+        # across launches as in a real run), when that table exists
+        try:
+            warm = json.load(open(p.replace("_traffic.json", "_traffic_warm.json")))["calls"]
+            for k, v in calls.items():
+                if k in warm:
+                    v["warm"] = warm[k]
+        except (OSError, KeyError, ValueError):
+            pass
+        return calls, os.path.relpath(p, ROOT)
     return {}, None
 
 

@@ -293,8 +293,17 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *   "block_div"    an SSSP round walks the blocked layout when its frontier
  *                  exceeds n / block_div (default 8, env FALCON_BLOCK_DIV;
  *                  0 = never)
- *   "pull_div"     BFS VERTEX runs bottom-up while the frontier exceeds
- *                  n / pull_div (default 16; 0 = never)
+ *   "pull_div"     BFS VERTEX may run bottom-up (over in-arcs)
+ *                  only while the frontier exceeds n / pull_div under rule
+ *                  1 / 2 (default 16; 0 = never pull)
+ *   "pull_rule"    BFS VERTEX direction per round: 0 = estimated L2 requests
+ *                  of a push and a pull round (default),
+ *                  1 / 2 = pull iff the frontier exceeds n / pull_div, with
+ *                  the word-per-warp / compacted pull form (env
+ *                  FALCON_BFS_PULL_RULE)
+ *   "cta_thr"      rows longer than this many arcs are expanded by the whole
+ *                  CTA instead of one warp (default 1024, env FALCON_CTA_THR;
+ *                  0 = warp-level only)
  *   "persist"      queue styles run small rounds in one cooperative kernel (0/1)
  *   "persist_max"  ... while the frontier holds at most this many items
  * Changing an option drops the cached CUDA graphs (and, for block_bytes, the

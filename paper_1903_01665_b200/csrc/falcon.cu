@@ -13,6 +13,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: one named range per C-ABI call (no link dependency)
 
+#include <atomic>
 #include <cstdarg>
 #include <map>
 #include <mutex>
@@ -206,7 +207,8 @@ struct falcon_graph {
     bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
     uint32_t cta_thr = 1024;             // CTA-level expansion of rows longer than this (FALCON_CTA_THR / option cta_thr; 0 = off)
-    uint32_t pull_unv4 = 0;              // BFS VERTEX: 1 = round-1 direction rule (pull iff frontier > n / pull_div)
+    uint32_t pull_rule = 0;              // BFS VERTEX direction: 0 cost model; 1 / 2 pull iff frontier > n / pull_div,
+                                         // word / compacted pull form (FALCON_BFS_PULL_RULE / option pull_rule)
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
     uint32_t split_div = 0;              // DELTA (auto Δ): halve the bucket when a near round hands on > n / split_div
                                          // items (FALCON_SPLIT_DIV; 0 = never)
@@ -239,9 +241,11 @@ struct falcon_graph {
     size_t mst_lcap = 0;
     // ---- views (graph_share): the parent's read-only arrays, own scratch ----
     falcon_graph *parent = nullptr;       // non-NULL: this handle is a view of `parent`
-    int nviews = 0;                       // (parent) live views
+    std::atomic<int> nviews{0};           // (parent) live views (graph_share / graph_free may run on other threads)
+    std::mutex unit_mu;                   // (root) guards the lazy build / publication of cw_unit
     // ---- a launched call not yet finished (run_launch / run_finish) ----
     int pend_algo = -1;
+    int32_t *pend_out = nullptr;          // pageable host output, copied by run_finish
     uint32_t pend_cap = 0;
     double pend_relax_ms = -1.0;
     int64_t pend_relax_launches = 0, pend_cc_passes = 0, pend_cc_launches = 0;
@@ -420,7 +424,7 @@ struct Round {
         launches++;
         launches++;
         k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n,
-                                                 STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div, g->pull_unv4,
+                                                 STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div, g->pull_rule,
                                                  (uint32_t)g->m);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
@@ -694,10 +698,14 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
     // (built on first use, 8 bytes per arc); the CUDA graph is cached in the
     // (BFS, DELTA) slot.  A view uses its parent's copy when there is one.
     falcon_graph *root = g->parent ? g->parent : g;
+    // cw_unit is read here by the root and its views, possibly from several
+    // host threads at once, and built by the root's first such call
+    std::unique_lock<std::mutex> unit_lock(root->unit_mu);
     const bool unit = algo == BFS && style == WORKLIST &&
                       (g->bfs_unit > 0 || (g->bfs_unit < 0 && g->local_tiles && g->m < 3 * g->n)) &&
                       (!g->parent || root->cw_unit);
     g->unit_run = unit;
+    if (!unit) unit_lock.unlock();
     if (unit) {
         style = DELTA;
         if (!root->cw_unit) {   // (only the root builds it; published once complete)
@@ -714,6 +722,7 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
             root->cw_unit = cu;
         }
         g->cw_unit = root->cw_unit;
+        unit_lock.unlock();
     }
     if (!g->parent) {   // a view shares layouts its parent built in graph_share
         if (style == EDGE) {
@@ -854,7 +863,14 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
     k_finish<<<1, BLOCK, 0, s>>>(a, (uint32_t)g->cnt_slots);
     CU(cudaGetLastError());
     CU(cudaEventRecord(g->ev1, s));
-    CU(cudaMemcpyAsync(out, g->val, (size_t)g->n * sizeof(int32_t), cudaMemcpyDefault, s));
+    // A copy into pageable host memory would block this thread until the call
+    // completes (falcon_run_many launches every job before waiting on any):
+    // it is deferred to run_finish.  Device and pinned outputs copy here.
+    cudaPointerAttributes pa{};
+    const bool pageable = cudaPointerGetAttributes(&pa, out) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered;
+    cudaGetLastError();   // (an unregistered pointer may leave an error on older runtimes)
+    g->pend_out = pageable ? out : nullptr;
+    if (!pageable) CU(cudaMemcpyAsync(out, g->val, (size_t)g->n * sizeof(int32_t), cudaMemcpyDefault, s));
     CU(cudaMemcpyAsync(g->h_ctrl, g->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     g->pend_algo = algo;
     g->pend_cap = cap;
@@ -888,6 +904,11 @@ falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats) {
     g->pend_algo = -1;
     CU(cudaSetDevice(g->device));
     CU(cudaStreamSynchronize(g->stream));
+    if (g->pend_out) {   // pageable host output (run_launch)
+        int32_t *o = g->pend_out;
+        g->pend_out = nullptr;
+        CU(cudaMemcpy(o, g->val, (size_t)g->n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
     const Ctrl &c = *g->h_ctrl;
     if (stats) {
         float ms = 0.f;
@@ -1125,7 +1146,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (const char *bd = getenv("FALCON_BLOCK_DIV")) g->blk_div = (uint32_t)atoi(bd);          // 0: never blocked
     const char *pd = getenv("FALCON_BFS_PULL_DIV");
     if (pd) g->pull_div = (uint32_t)atoi(pd);
-    if (const char *pu = getenv("FALCON_BFS_PULL_UNV")) g->pull_unv4 = (uint32_t)atoi(pu);
+    if (const char *pu = getenv("FALCON_BFS_PULL_RULE")) g->pull_rule = (uint32_t)atoi(pu);
     if (const char *ct = getenv("FALCON_CTA_THR")) g->cta_thr = (uint32_t)atoi(ct);
     int slots = g->grid_persist;
     for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_edge_b, g->grid_small, g->grid_cc,
@@ -1203,7 +1224,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->dl_noq = p->dl_noq; v->split_div = p->split_div; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
     v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
-    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_unv4 = p->pull_unv4; v->cta_thr = p->cta_thr;
+    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_rule = p->pull_rule; v->cta_thr = p->cta_thr;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
     v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
     v->grid_pull = p->grid_pull; v->grid_cc = p->grid_cc; v->grid_edge = p->grid_edge; v->grid_edge_b = p->grid_edge_b;
@@ -1273,7 +1294,7 @@ falcon_status_t graph_load_csr(int64_t n, int64_t m, const uint32_t *row_off, co
 }
 
 falcon_status_t graph_free(falcon_graph_t *g) {
-    if (g && g->nviews > 0) return fail(FALCON_ERR_INVALID_ARG, "graph has %d live views (free them first)", g->nviews);
+    if (g && g->nviews > 0) return fail(FALCON_ERR_INVALID_ARG, "graph has %d live views (free them first)", g->nviews.load());
     destroy(g);
     return FALCON_OK;
 }
@@ -1508,8 +1529,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->pull_div = (uint32_t)value;
         } else if (!strcmp(name, "cta_thr")) {
             t->cta_thr = (uint32_t)value;
-        } else if (!strcmp(name, "pull_unv")) {
-            t->pull_unv4 = (uint32_t)value;
+        } else if (!strcmp(name, "pull_rule")) {
+            t->pull_rule = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {
             if (value && t->grid_persist <= 0) return fail(FALCON_ERR_UNSUPPORTED, "cooperative launch unavailable");
             t->persist = value != 0;

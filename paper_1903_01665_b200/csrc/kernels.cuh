@@ -1392,12 +1392,13 @@ __global__ void k_compress(Args a) {
 //   pull ~ 2U (in-arc offsets and first in-arcs of each unvisited vertex)
 //          + U min(m/n, m/m_f) (in-arcs scanned until a parent: 1/p with
 //          p = m_f/m the frontier's share of the in-arcs).
-// pull_div keeps the round-1 rule instead (pull iff F > n / pull_div) when
-// unv4 is set to 1 (FALCON_BFS_PULL_UNV=1).  Only the schedule changes.
+// rule 1 / 2 (option pull_rule) keeps the round-1 rule instead -- pull iff
+// F > n / pull_div -- with the word / compacted form.  Only the schedule
+// changes, never the levels.
 __device__ __forceinline__ uint32_t bfs_direction(const Ctrl *c, uint32_t n, uint64_t m, uint32_t pull_div,
-                                                  uint32_t unv4) {
+                                                  uint32_t rule) {
     if (!pull_div || c->found == 0) return 0;
-    if (unv4 == 1) return c->found > n / pull_div ? 1u : 0u;
+    if (rule == 1 || rule == 2) return c->found > n / pull_div ? rule : 0u;
     const float F = (float)c->found, U = (float)(n - c->visited), N = (float)n, M = (float)m;
     if (c->found <= n / 1024u) return 0;   // small frontier: push
     const float d = !c->pull && c->rnd_items ? (float)c->rnd_edges / (float)c->rnd_items : M / N;
@@ -1414,7 +1415,7 @@ __device__ __forceinline__ uint32_t bfs_direction(const Ctrl *c, uint32_t n, uin
 // aux_div: BFS VERTEX: pull_div (bottom-up threshold); DELTA: split_div (bucket split)
 template <int ALGO, int STYLE>
 __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t aux_div,
-                                             uint32_t blk_div, uint32_t unv4 = 0, uint64_t m = 0) {
+                                             uint32_t blk_div, uint32_t rule = 0, uint64_t m = 0) {
     const uint32_t pull_div = aux_div;
     if (c->done) return false;
     c->launches += launches_per_round;
@@ -1487,7 +1488,7 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             // direction-optimising BFS: bottom-up while the next frontier is large
             if (ALGO == BFS) {
                 c->visited += c->found;
-                c->pull = bfs_direction(c, n, m, pull_div, unv4);
+                c->pull = bfs_direction(c, n, m, pull_div, rule);
                 c->rnd_items = 0;
                 c->rnd_edges = 0;
             }
@@ -1507,9 +1508,9 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
 __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
-                          uint32_t n, uint32_t pull_div, uint32_t blk_div, uint32_t unv4, uint32_t m) {
+                          uint32_t n, uint32_t pull_div, uint32_t blk_div, uint32_t rule, uint32_t m) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div, unv4, m);
+    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div, rule, m);
     if (in_graph) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
