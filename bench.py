@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--impl", default="falcon", choices=["falcon", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-mode", default="many", choices=["many", "calls"],
+                    help="e2e step: falcon_run_many over graph views (every job in flight, each result's D2H "
+                         "overlapping the other jobs) or one blocking call after another")
     ap.add_argument("--no-classes", action="store_true", help="skip the per-class best-style roofline (rmat-10M)")
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--mode", default=None, choices=["replica", "sections", "partition"],
@@ -572,13 +575,23 @@ def main():
         else:
             h_ro, h_col, h_w = pin(G.row_off), pin(G.col), pin(G.w)
             e_n, e_m, e_flags = G.n, G.m, 0
-        h_out = torch.empty(g.out_len, dtype=torch.int32).pin_memory()
+        many = args.e2e_mode == "many" and not partition   # (partitioned graphs have no views)
+        h_outs = [torch.empty(g.out_len, dtype=torch.int32).pin_memory() for _ in (runs if many else runs[:1])]
         e_steps = max(1, min(args.steps, 3))
 
         def e2e_step():
             gh = fb.graph_load_csr(e_n, e_m, h_ro, h_col, h_w, device=local, stream=stream, comm=comm, flags=e_flags)
-            for a, s in runs:
-                fb.run(gh, a, s, h_out, G.source)
+            if many:
+                # the public concurrent-call API: one view per job,
+                # every job launched before any is waited on, results copied to pinned
+                # host buffers on the views' own streams
+                hs = [gh] + [fb.graph_share(gh) for _ in runs[1:]]
+                fb.falcon_run_many([(h, a, s, G.source, o) for h, (a, s), o in zip(hs, runs, h_outs)])
+                for h in hs[1:]:
+                    fb.graph_free(h)
+            else:
+                for a, s in runs:
+                    fb.run(gh, a, s, h_outs[0], G.source)
             fb.graph_free(gh)
 
         e2e_step()
@@ -598,7 +611,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": replicas * units_per_step * e_steps / (ems * 1e-3) / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": 4 * (e_n + 1) + 8 * e_m, "d2h_bytes_per_step": 4 * g.out_len * len(runs),
-               "steps": e_steps, "ms_per_step": ems / e_steps}
+               "steps": e_steps, "ms_per_step": ems / e_steps,
+               "mode": "falcon_run_many over graph views" if many else "one falcon_* call after another"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

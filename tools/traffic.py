@@ -4,7 +4,8 @@ roofline blocks.
 
   1. on the GPU box, under ncu (one GPU):
        ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors.sum,\
-lts__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none --csv --log-file gpurun_out/traffic.csv \
+lts__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum,\
+lts__t_sectors_op_read.sum,lts__t_sector_hit_rate.pct --clock-control none --csv --log-file gpurun_out/traffic.csv \
            python tools/traffic.py run --out gpurun_out/traffic_stats.json
      (one call per (class, algo, style) in profiling mode; every call ends
      with exactly one k_finish launch, which delimits the calls in the list)
@@ -64,6 +65,10 @@ def combine(csv_path, stats_path):
         dram = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for _, d in c)
         t_us = sum(d.get("gpu__time_duration.sum", 0) for _, d in c)
         sect = sum(d.get("lts__t_sectors.sum", 0) for _, d in c)
+        atom = sum(d.get("lts__t_sectors_op_atom.sum", 0) for _, d in c)
+        red = sum(d.get("lts__t_sectors_op_red.sum", 0) for _, d in c)
+        rd = sum(d.get("lts__t_sectors_op_read.sum", 0) for _, d in c)
+        hit = [d.get("lts__t_sector_hit_rate.pct", 0) for _, d in c]
         lts = [d.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", 0) for _, d in c]
         wts = [d.get("gpu__time_duration.sum", 0) for _, d in c]
         key = f"{s['class']}:{s['algo']}/{s['style']}"
@@ -72,6 +77,10 @@ def combine(csv_path, stats_path):
                     "ncu_relax_us": t_us,
                     "lts_throughput_pct_time_weighted": sum(a * b for a, b in zip(lts, wts)) / max(1e-9, sum(wts)),
                     "lts_throughput_pct_max": max(lts) if lts else 0.0,
+                    "lts_sectors_read": rd, "lts_sectors_atom": atom, "lts_sectors_red": red,
+                    "lts_hit_pct_time_weighted": sum(a * b for a, b in zip(hit, wts)) / max(1e-9, sum(wts)),
+                    "edges_relaxed": s["stats"]["edges_relaxed"], "updates": s["stats"]["updates"],
+                    "lts_sectors_per_relaxed_arc": sect / max(1, s["stats"]["edges_relaxed"]),
                     "kernels": sorted({nm.split("(")[0] for nm, _ in c})}
     print(json.dumps({"source": "ncu --metrics (cold-cache, serialised; one call per key in profiling mode): "
                                 "tools/traffic.py", "calls": out}, indent=1))
