@@ -183,6 +183,15 @@ CONFIGS = {
     "rmat-50M": lambda: rmat(50_000_000, 500_000_000, 50, name="rmat-50M"),
 }
 
+# The partner graphs of the paper's multi-target experiment (Table 1 sizes,
+# PAPER.md:24-35; Tables tab:multigpucc / tab:multigpubfs):
+# rand-50M, rmat-20M, and a USA-CTR-shaped road grid (14M vertices / 34M arcs).
+PAIR_CONFIGS = {
+    "rand-50M": lambda: er(50_000_000, 200_000_000, 50, name="rand-50M"),
+    "rmat-20M": lambda: rmat(20_000_000, 200_000_000, 20, name="rmat-20M"),
+    "grid-14M": lambda: grid(4000, 3500, 14, name="grid-14M"),
+}
+
 # Reduced-scale analogues with the same recipe (for tests that must run fast).
 SMALL_CONFIGS = {
     "rand-s": lambda: er(200_000, 800_000, 125, name="rand-s"),
@@ -196,6 +205,8 @@ def config(name: str) -> Graph:
         return CONFIGS[name]()
     if name in SMALL_CONFIGS:
         return SMALL_CONFIGS[name]()
+    if name in PAIR_CONFIGS:
+        return PAIR_CONFIGS[name]()
     raise KeyError(name)
 
 
