@@ -371,13 +371,19 @@ void launch_expand_warp(const falcon_graph *g, cudaStream_t s, const Args &a) {
     case 2: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 3>, g->grid_expand_fr, s, a); break;
     case 3: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 6>, g->grid_expand_fr, s, a); break;
     case 4: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 8, 2>, g->grid_expand_fr, s, a); break;
+    case 5: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 4>, g->grid_expand_dl, s, a); break;
+    case 6: launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 3, 4>, g->grid_expand_dl, s, a); break;
     default:   // tuned per style (tools/survey.py sweeps on rand-25M / rmat-10M)
         // DELTA: U = 4 / 3 CTAs per SM where rounds are heavy (rand-25M 3.38 -> 3.08 ms,
         // rmat-10M 4.39 -> 3.14 ms against U = 2 / 4 CTAs), U = 2 / 4 CTAs on sparse
         // high-diameter graphs, whose small local-continuation rounds want the warps
         // (grid-24M 41 ms against 66 ms with U = 4)
+        // BFS VERTEX: U = 4 fits 64 registers without spills: 4 CTAs per SM
+        // (rand-25M 1.011 -> 0.981 ms; SSSP spills at that bound)
         if (STYLE == DELTA && g->m < 3 * g->n)
             launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 2, 4>, g->grid_expand_dl, s, a);
+        else if (ALGO == BFS && STYLE == VERTEX)
+            launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 4>, g->grid_expand_dl, s, a);
         else
             launch_l2(g, k_expand_warp<ALGO, STYLE, BLOCK, 4, 3>, g->grid_expand_fr, s, a);
         break;
@@ -1103,8 +1109,8 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     int occ_f = 0, occ_e = 0, occ_p = 0;
     const char *var = getenv("FALCON_EXPAND_VARIANT");
     g->variant = var ? atoi(var) : 0;
-    static const int var_minb[5] = {3, 4, 3, 6, 2};
-    occ_f = var_minb[g->variant >= 0 && g->variant < 5 ? g->variant : 0];
+    static const int var_minb[7] = {3, 4, 3, 6, 2, 4, 4};
+    occ_f = var_minb[g->variant >= 0 && g->variant < 7 ? g->variant : 0];
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_persist<SSSP, DELTA, BLOCK, UNROLL>, BLOCK, 0));
     {
         int o2 = 0;
