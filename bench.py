@@ -524,6 +524,9 @@ def main():
         for a, s_ in runs:
             fb.run(g, a, s_, out, G.source)
             np.save(os.path.join(args.dump, f"rank{rank}_{a}_{s_}.npy"), out.cpu().numpy())
+        if comm is not None:   # this rank's output is its owned slice [lo, hi) (the full array when simulated)
+            json.dump({"lo": int(glo), "hi": int(ghi), "len": int(g.out_len)},
+                      open(os.path.join(args.dump, f"rank{rank}_range.json"), "w"))
         if rank == 0:
             json.dump({"config": args.config, "mode": args.mode, "world": world, "source": int(G.source),
                        "runs": [list(r) for r in all_runs]}, open(os.path.join(args.dump, "meta.json"), "w"))
