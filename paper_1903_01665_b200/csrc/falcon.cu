@@ -206,6 +206,8 @@ struct falcon_graph {
     int32_t bfs_unit = -1;               // BFS WORKLIST as unit-weight Δ-stepping: -1 auto (m < 3n), 0 off, 1 on
     bool unit_run = false;               // the call in flight is such a BFS: arcs from cw_unit
     uint32_t *rin_off = nullptr, *rin_col = nullptr;   // reverse CSR (BFS pull), built lazily
+    uint32_t lazy_div = 256;             // BFS VERTEX lazy visited set in push rounds with frontier > n / lazy_div
+                                         // (option bfs_lazy_div / FALCON_BFS_LAZY_DIV; 0 = never)
     uint32_t cta_thr = 1024;             // CTA-level expansion of rows longer than this (FALCON_CTA_THR / option cta_thr; 0 = off)
     uint32_t pull_rule = 0;              // BFS VERTEX direction: 0 cost model; 1 / 2 pull iff frontier > n / pull_div,
                                          // word / compacted pull form (FALCON_BFS_PULL_RULE / option pull_rule)
@@ -431,7 +433,7 @@ struct Round {
         launches++;
         k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n,
                                                  STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div, g->pull_rule,
-                                                 (uint32_t)g->m);
+                                                 (uint32_t)g->m, g->lazy_div);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
     }
@@ -1154,6 +1156,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     if (const char *pu = getenv("FALCON_BFS_PULL_RULE")) g->pull_rule = (uint32_t)atoi(pu);
     if (const char *ct = getenv("FALCON_CTA_THR")) g->cta_thr = (uint32_t)atoi(ct);
+    if (const char *lv = getenv("FALCON_BFS_LAZY_DIV")) g->lazy_div = (uint32_t)atoi(lv);
     int slots = g->grid_persist;
     for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_edge_b, g->grid_small, g->grid_cc,
                     g->grid_pull})
@@ -1230,7 +1233,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->dense_div = p->dense_div; v->blk_div = p->blk_div; v->wl_noq = p->wl_noq; v->dl_noq = p->dl_noq; v->split_div = p->split_div; v->local_tiles = p->local_tiles; v->local_max = p->local_max;
     v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
-    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_rule = p->pull_rule; v->cta_thr = p->cta_thr;
+    v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_rule = p->pull_rule; v->cta_thr = p->cta_thr; v->lazy_div = p->lazy_div;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
     v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
     v->grid_pull = p->grid_pull; v->grid_cc = p->grid_cc; v->grid_edge = p->grid_edge; v->grid_edge_b = p->grid_edge_b;
@@ -1533,6 +1536,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->wl_local_max = (uint32_t)std::min<int64_t>(value, 0xffffffffll);
         } else if (!strcmp(name, "pull_div")) {
             t->pull_div = (uint32_t)value;
+        } else if (!strcmp(name, "bfs_lazy_div")) {
+            t->lazy_div = (uint32_t)value;
         } else if (!strcmp(name, "cta_thr")) {
             t->cta_thr = (uint32_t)value;
         } else if (!strcmp(name, "pull_rule")) {

@@ -60,6 +60,10 @@ struct Ctrl {
     uint32_t found;       // BFS: vertices discovered this round (direction heuristic)
     uint32_t visited;     // BFS: vertices discovered so far (direction heuristic)
     unsigned long long rnd_items, rnd_edges;   // BFS VERTEX: items expanded / arcs scanned this round
+    uint32_t lazy;        // BFS VERTEX: this push round marks discoveries in the round bitmap only
+    uint32_t merge;       // BFS VERTEX: last round was lazy -- its discoveries are not in vis yet
+    uint32_t lazy_found;  // BFS VERTEX: `found` of the last lazy round (counts a vertex once per marking arc)
+    uint32_t exact;       // BFS VERTEX: its discoveries counted exactly while they are merged into vis
     uint32_t thr;         // DELTA: current bucket threshold T (near: dist < T)
     uint32_t delta;       // DELTA: bucket width
     uint32_t minpend;     // DELTA: min tentative distance parked in the far set
@@ -106,6 +110,8 @@ struct Args {
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
     uint32_t dl_noq;           // ... DELTA dense rounds (near marks in the bitmap, far parking as usual)
     uint32_t cta_thr;          // rows longer than this are expanded by the whole CTA (0: warp-level only)
+    uint32_t lazy_div;         // BFS VERTEX: a push round whose frontier exceeds n / lazy_div marks only the
+                               // round bitmap; the next round's k_pull merges it into vis (0: never)
     // fused partitioned rounds (VFUSED): owned range, part bounds and the
     // owners' value arrays / round bitmaps (peer memory on real GPUs)
     uint32_t lo, hi, nparts;
@@ -325,7 +331,7 @@ __global__ void k_init(Args a, uint32_t source, uint32_t cap, uint32_t cnt_len, 
         c->all_active = ALGO == CC ? 1u : 0u;
         c->status = ST_OK; c->source = source;
         c->launches = 1; c->vertices = 0; c->edges = 0; c->updates = 0;
-        c->pull = 0; c->found = 0; c->visited = 1; c->rnd_items = 0; c->rnd_edges = 0;
+        c->pull = 0; c->found = 0; c->visited = 1; c->rnd_items = 0; c->rnd_edges = 0; c->lazy = 0; c->merge = 0; c->lazy_found = 0; c->exact = 0;
         c->thr = delta; c->delta = delta; c->minpend = 0xffffffffu; c->mode = MODE_NEAR;
         c->delta0 = delta; c->delta_adapt = a.delta_adapt; c->bk_rounds = 0; c->bk_items = 0;
         c->delta_cap = a.delta_cap ? a.delta_cap : 128u;
@@ -455,20 +461,47 @@ __global__ void k_sum_weights(uint64_t m, const int32_t *w, unsigned long long *
 template <int B>
 __global__ void __launch_bounds__(B) k_pull(Args a) {
     Ctrl *c = a.ctrl;
-    if (c->done || !c->pull) return;
+    if (c->done) return;
+    if (!c->pull) {
+        // lazy visited set (Ctrl::lazy): a heavy push round sets only the
+        // round bitmap; the vertices it discovered join the visited bitmap
+        // here, before the next round's expansion tests it
+        if (c->merge) {
+            const uint4 *p4 = reinterpret_cast<const uint4 *>(bm_of(a, c->iter - 1));
+            uint4 *v4 = reinterpret_cast<uint4 *>(a.vis);
+            uint32_t fresh = 0;
+            for (uint32_t i = blockIdx.x * B + threadIdx.x; i < a.nwords / 4; i += gridDim.x * B) {
+                const uint4 p = p4[i];
+                if (p.x | p.y | p.z | p.w) {
+                    uint4 v = v4[i];
+                    fresh += __popc(p.x & ~v.x) + __popc(p.y & ~v.y) + __popc(p.z & ~v.z) + __popc(p.w & ~v.w);
+                    v.x |= p.x; v.y |= p.y; v.z |= p.z; v.w |= p.w;
+                    v4[i] = v;
+                }
+            }
+            fresh = __reduce_add_sync(FULL, fresh);
+            if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(&c->exact, fresh);
+        }
+        return;
+    }
     const uint32_t iter = c->iter, lev = iter - 1;
     clear_next_bitmap(a, iter);
     const uint32_t *bm_prev = bm_of(a, iter - 1);
     uint32_t *bm_now = bm_of(a, iter);
+    const bool merge = c->merge != 0;   // (vis lacks last round's discoveries: visw |= prevw below, written back)
     if (c->pull == 1) {
         const int lane = threadIdx.x & 31;
+        uint32_t fresh = 0;   // last (lazy) round's discoveries, counted once each
         const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
         unsigned long long nv = 0, ne = 0, nu = 0;
         bool chg = false;
         for (uint32_t wi = gw; wi < a.nwords; wi += nwarps) {
-            const uint32_t visw = a.vis[wi];
+            const uint32_t prevw = bm_prev[wi];
+            const uint32_t vis0 = a.vis[wi];
+            const uint32_t visw = vis0 | prevw;   // (a lazy visited set lacks last round's discoveries)
+            if (merge && lane == 0) fresh += __popc(prevw & ~vis0);
             const uint32_t v = wi * 32u + lane;
-            if ((bm_prev[wi] >> lane) & 1u) put_level(a, v, lev);   // discovered last round
+            if ((prevw >> lane) & 1u) put_level(a, v, lev);   // discovered last round
             bool found = false;
             if (v < a.n && !((visw >> lane) & 1u)) {
                 nv++;
@@ -479,11 +512,15 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
                 }
             }
             const unsigned mask = __ballot_sync(FULL, found);
-            if (mask && lane == 0) {
-                a.vis[wi] = visw | mask;
-                bm_now[wi] = mask;
+            if (lane == 0) {
+                if (mask || (merge && prevw)) a.vis[wi] = visw | mask;
+                if (mask) bm_now[wi] = mask;
             }
             if (found) { nu++; chg = true; }
+        }
+        if (merge) {
+            fresh = __reduce_add_sync(FULL, fresh);
+            if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(&c->exact, fresh);
         }
         flush_counters<B>(a, nv, ne, nu, chg, false);
         return;
@@ -499,10 +536,16 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
     const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
     unsigned long long nv = 0, ne = 0, nu = 0;
     bool chg = false;
+    uint32_t fresh = 0;
     for (uint32_t g0 = gw * PG; g0 < a.nwords; g0 += nwarps * PG) {   // warp-uniform
         const uint32_t wi = g0 + lane;
         uint32_t visw = 0xffffffffu, prevw = 0;
-        if (lane < PG && wi < a.nwords) { visw = a.vis[wi]; prevw = bm_prev[wi]; }
+        if (lane < PG && wi < a.nwords) {
+            prevw = bm_prev[wi];
+            const uint32_t vis0 = a.vis[wi];
+            visw = vis0 | prevw;
+            if (merge) fresh += __popc(prevw & ~vis0);
+        }
         // the level of the vertices discovered last round: one coalesced
         // 128-byte store per non-empty word
         for (unsigned pm = __ballot_sync(FULL, prevw != 0); pm; pm &= pm - 1) {   // warp-uniform
@@ -549,6 +592,7 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
         }
         __syncwarp();
         const uint32_t nw = lane < PG ? sfd[lane] : 0u;
+        if (merge && prevw && !nw && lane < PG) a.vis[wi] = visw;   // last round's discoveries join
         if (nw) {
             a.vis[wi] = visw | nw;
             bm_now[wi] = nw;
@@ -556,6 +600,10 @@ __global__ void __launch_bounds__(B) k_pull(Args a) {
             chg = true;
         }
         __syncwarp();
+    }
+    if (merge) {
+        fresh = __reduce_add_sync(FULL, fresh);
+        if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(&c->exact, fresh);
     }
     flush_counters<B>(a, nv, ne, nu, chg, false);
 }
@@ -626,6 +674,7 @@ struct Xw {
     // (shared list hb/hd/hp of HMAX rows, count *hn; hthr = 0: off)
     uint32_t *hb, *hd, *hp, *hn;
     uint32_t hthr;
+    bool lazy;   // BFS VERTEX lazy push round (Ctrl::lazy)
 };
 constexpr uint32_t HMAX = 64;   // long rows per CTA and round (more: the warp expands them itself)
 
@@ -770,7 +819,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
                 if (QUEUE) {   // the queue needs exactly-once: claim
                     need[q] = true; citem[q] = s.v[q];
                 } else {   // VERTEX: the level is written when the vertex is expanded next round
-                    atomicOr(a.vis + (s.v[q] >> 5), 1u << (s.v[q] & 31));
+                    if (!(is_vertex(STYLE) && x.lazy)) atomicOr(a.vis + (s.v[q] >> 5), 1u << (s.v[q] & 31));
                     atomicOr(x.bm_now + (s.v[q] >> 5), 1u << (s.v[q] & 31));
                     if (NOQ) put_level(a, s.v[q], x.lev + 1);
                     acc.nu++; acc.chg = true;
@@ -971,6 +1020,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
     x.bm_now = bm_of(a, iter); x.bm_prev = bm_of(a, iter - 1); x.out = out; x.wq = wq; x.c = c;
     x.lev = iter - 1; x.thr = thr; x.qh = 0; x.qn = 0; x.pend_min = 0xffffffffu;
     x.pf = pol_evict_first(); x.pl = pol_evict_last();
+    x.lazy = ALGO == BFS && is_vertex(STYLE) && c->lazy;
     x.hthr = heavy && !COHERENT ? a.cta_thr : 0u;   // heavy: the CTA's shared long-row list
     if (x.hthr) { x.hn = heavy; x.hb = heavy + 1; x.hd = heavy + 1 + HMAX; x.hp = heavy + 1 + 2 * HMAX; }
     blocked = blocked && ALGO == SSSP && a.nblk > 1;
@@ -1399,7 +1449,7 @@ __device__ __forceinline__ uint32_t bfs_direction(const Ctrl *c, uint32_t n, uin
                                                   uint32_t rule) {
     if (!pull_div || c->found == 0) return 0;
     if (rule == 1 || rule == 2) return c->found > n / pull_div ? rule : 0u;
-    const float F = (float)c->found, U = (float)(n - c->visited), N = (float)n, M = (float)m;
+    const float F = (float)c->found, U = c->visited >= n ? 0.f : (float)(n - c->visited), N = (float)n, M = (float)m;
     if (c->found <= n / 1024u) return 0;   // small frontier: push
     const float d = !c->pull && c->rnd_items ? (float)c->rnd_edges / (float)c->rnd_items : M / N;
     const float mf = F * d;
@@ -1415,7 +1465,8 @@ __device__ __forceinline__ uint32_t bfs_direction(const Ctrl *c, uint32_t n, uin
 // aux_div: BFS VERTEX: pull_div (bottom-up threshold); DELTA: split_div (bucket split)
 template <int ALGO, int STYLE>
 __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_round, uint32_t n, uint32_t aux_div,
-                                             uint32_t blk_div, uint32_t rule = 0, uint64_t m = 0) {
+                                             uint32_t blk_div, uint32_t rule = 0, uint64_t m = 0,
+                                             uint32_t lazy_div = 0) {
     const uint32_t pull_div = aux_div;
     if (c->done) return false;
     c->launches += launches_per_round;
@@ -1487,8 +1538,15 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             c->in_len = 0;   // VERTEX rounds read the activity bitmap
             // direction-optimising BFS: bottom-up while the next frontier is large
             if (ALGO == BFS) {
+                // a lazy round counted a vertex once per marking arc; the round
+                // after it counted them exactly while merging them into vis
+                if (c->merge) c->visited = c->visited - c->lazy_found + c->exact;
                 c->visited += c->found;
+                c->merge = c->lazy;   // a lazy round's discoveries join vis in the next round's k_pull
+                c->lazy_found = c->found;
+                c->exact = 0;
                 c->pull = bfs_direction(c, n, m, pull_div, rule);
+                c->lazy = !c->pull && lazy_div && c->found > n / lazy_div;
                 c->rnd_items = 0;
                 c->rnd_edges = 0;
             }
@@ -1508,9 +1566,10 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
 // CUDA-graph WHILE node through cudaGraphSetConditional.
 template <int ALGO, int STYLE>
 __global__ void k_advance(Ctrl *c, cudaGraphConditionalHandle h, int in_graph, uint32_t launches_per_round,
-                          uint32_t n, uint32_t pull_div, uint32_t blk_div, uint32_t rule, uint32_t m) {
+                          uint32_t n, uint32_t pull_div, uint32_t blk_div, uint32_t rule, uint32_t m,
+                          uint32_t lazy_div) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div, rule, m);
+    const bool more = advance_step<ALGO, STYLE>(c, launches_per_round, n, pull_div, blk_div, rule, m, lazy_div);
     if (in_graph) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 

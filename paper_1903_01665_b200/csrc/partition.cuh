@@ -791,9 +791,9 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
             }
             for (size_t i = 0; i < g->parts.size(); i++) {
                 if (algo == CC)
-                    k_advance<CC, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u, 0u, 0u, 0u);
+                    k_advance<CC, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u, 0u, 0u, 0u, 0u);
                 else
-                    k_advance<SSSP, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u, 0u, 0u, 0u);
+                    k_advance<SSSP, VERTEX><<<1, 32, 0, s>>>(g->parts[i]->ctrl, 0, 0, 0u, (uint32_t)g->n, 0u, 0u, 0u, 0u, 0u);
             }
         }
         CU(cudaGetLastError());

@@ -1,4 +1,4 @@
-"""A/B one library option on one loaded graph (same box, same graph, interleaved reps).
+"""A/B one library option on the same graph (same box, one handle per value, interleaved reps).
 
 python tools/option_ab.py --config rmat-10M --algos sssp,bfs --styles vertex,worklist --option cta_thr=0,1024
 Configs: the graphgen names, er:n:m:seed, rmat:n:m:seed, star:n (a hub with n-1 out-arcs, every leaf
@@ -49,8 +49,13 @@ vals = [int(v) for v in vals.split(",")]
 t = time.time()
 G = make(a.config)
 print(f"== {a.config}: n={G.n} m={G.m} gen {time.time() - t:.1f}s  option {name} in {vals}", flush=True)
-g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, stream=torch.cuda.current_stream(),
-                      flags=fb.LOAD_BUILD_COO)
+# one handle per option value (setting an option drops the handle's cached
+# CUDA graphs, so switching one handle back and forth would time captures)
+hs = {}
+for v in vals:
+    hs[v] = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0, stream=torch.cuda.current_stream(),
+                              flags=fb.LOAD_BUILD_COO)
+    fb.falcon_set_option(hs[v], name, v)
 out = torch.empty(G.n, dtype=torch.int32, device="cuda")
 for algo in a.algos.split(","):
     for style in a.styles.split(","):
@@ -58,10 +63,9 @@ for algo in a.algos.split(","):
             continue
         ms = {v: [] for v in vals}
         ref = None
-        for r in range(a.reps + 1):
+        for r in range(a.reps + 1):   # rep 0: warm-up (layouts, CUDA graph capture)
             for v in vals:
-                fb.falcon_set_option(g, name, v)
-                st = fb.run(g, algo, style, out, G.source)
+                st = fb.run(hs[v], algo, style, out, G.source)
                 if r:
                     ms[v].append(st.ms)
                 res = out.cpu().numpy().copy()
@@ -70,4 +74,5 @@ for algo in a.algos.split(","):
                 assert np.array_equal(res, ref), f"{algo}/{style}: {name}={v} changed the result"
         line = "  ".join(f"{name}={v}: {statistics.median(ms[v]):8.3f}" for v in vals)
         print(f"{a.config:10s} {algo:4s} {style:8s} {line}  ms (median of {a.reps})", flush=True)
-fb.graph_free(g)
+for v in vals:
+    fb.graph_free(hs[v])
