@@ -304,6 +304,10 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *   "cta_thr"      rows longer than this many arcs are expanded by the whole
  *                  CTA instead of one warp (default 1024, env FALCON_CTA_THR;
  *                  0 = warp-level only)
+ *   "skip_now"     SSSP expansion styles: an item whose bit is already set in
+ *                  the current round's bitmap (improved again this round, so
+ *                  it is expanded next round with its newer value) is not
+ *                  expanded now (default 1, env FALCON_SKIP_NOW; 0 = off)
  *   "persist"      queue styles run small rounds in one cooperative kernel (0/1)
  *   "persist_max"  ... while the frontier holds at most this many items
  * Changing an option drops the cached CUDA graphs (and, for block_bytes, the

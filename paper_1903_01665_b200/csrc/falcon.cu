@@ -209,6 +209,8 @@ struct falcon_graph {
     uint32_t lazy_div = 256;             // BFS VERTEX lazy visited set in push rounds with frontier > n / lazy_div
                                          // (option bfs_lazy_div / FALCON_BFS_LAZY_DIV; 0 = never)
     uint32_t cta_thr = 1024;             // CTA-level expansion of rows longer than this (FALCON_CTA_THR / option cta_thr; 0 = off)
+    uint32_t skip_now = 1;               // SSSP: an item already re-activated for the next round is not expanded now
+                                         // (FALCON_SKIP_NOW / option skip_now; 0 = off)
     uint32_t pull_rule = 0;              // BFS VERTEX direction: 0 cost model; 1 / 2 pull iff frontier > n / pull_div,
                                          // word / compacted pull form (FALCON_BFS_PULL_RULE / option pull_rule)
     uint32_t pull_div = 16;              // BFS VERTEX: bottom-up when next frontier > n / pull_div (0 = never)
@@ -295,6 +297,7 @@ struct falcon_graph {
         a.wl_noq = wl_noq;
         a.dl_noq = dl_noq;
         a.cta_thr = cta_thr;
+        a.skip_now = skip_now;
         a.local_tiles = local_tiles;
         a.local_max = local_max;
         a.wl_local_tiles = wl_local_tiles;
@@ -1156,6 +1159,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (pd) g->pull_div = (uint32_t)atoi(pd);
     if (const char *pu = getenv("FALCON_BFS_PULL_RULE")) g->pull_rule = (uint32_t)atoi(pu);
     if (const char *ct = getenv("FALCON_CTA_THR")) g->cta_thr = (uint32_t)atoi(ct);
+    if (const char *sn = getenv("FALCON_SKIP_NOW")) g->skip_now = (uint32_t)atoi(sn);
     if (const char *lv = getenv("FALCON_BFS_LAZY_DIV")) g->lazy_div = (uint32_t)atoi(lv);
     int slots = g->grid_persist;
     for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_edge_b, g->grid_small, g->grid_cc,
@@ -1234,6 +1238,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
     v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_rule = p->pull_rule; v->cta_thr = p->cta_thr; v->lazy_div = p->lazy_div;
+    v->skip_now = p->skip_now;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
     v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
     v->grid_pull = p->grid_pull; v->grid_cc = p->grid_cc; v->grid_edge = p->grid_edge; v->grid_edge_b = p->grid_edge_b;
@@ -1540,6 +1545,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->lazy_div = (uint32_t)value;
         } else if (!strcmp(name, "cta_thr")) {
             t->cta_thr = (uint32_t)value;
+        } else if (!strcmp(name, "skip_now")) {
+            t->skip_now = (uint32_t)value;
         } else if (!strcmp(name, "pull_rule")) {
             t->pull_rule = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {

@@ -110,6 +110,8 @@ struct Args {
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
     uint32_t dl_noq;           // ... DELTA dense rounds (near marks in the bitmap, far parking as usual)
     uint32_t cta_thr;          // rows longer than this are expanded by the whole CTA (0: warp-level only)
+    uint32_t skip_now;         // SSSP: an item whose bit is already set in this round's bitmap (improved again
+                               // this round, so expanded next round with its newer value) is not expanded now
     uint32_t lazy_div;         // BFS VERTEX: a push round whose frontier exceeds n / lazy_div marks only the
                                // round bitmap; the next round's k_pull merges it into vis (0: never)
     // fused partitioned rounds (VFUSED): owned range, part bounds and the
@@ -1044,11 +1046,16 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
             for (int k = 0; k < DP; k++) wq[k] = word_at(gw * 32 + k * wstride + lane);
             for (uint32_t g0 = gw * 32; g0 < a.nwords; g0 += wstride) {   // warp-uniform
                 const uint32_t wi = g0 + lane;
-                const uint32_t word = wq[0];
+                const uint32_t word0 = wq[0];
 #pragma unroll
                 for (int k = 0; k < DP - 1; k++) wq[k] = wq[k + 1];
                 wq[DP - 1] = word_at(g0 + DP * wstride + lane);
-                if (!__any_sync(FULL, word != 0u)) continue;
+                if (!__any_sync(FULL, word0 != 0u)) continue;
+                if (QUEUE && last && word0) x.bm_prev[wi] = 0u;   // recycle the claim bitmap
+                // skip_now: items already marked for the next round wait for it
+                // (their expansion now would use a value the next one supersedes)
+                uint32_t word = word0;
+                if (ALGO == SSSP && a.skip_now && word) word &= ~(COHERENT ? __ldcg(x.bm_now + wi) : x.bm_now[wi]);
                 const uint32_t cnt = __popc(word);
                 uint32_t incl = cnt;
 #pragma unroll
@@ -1060,7 +1067,6 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                 if (total == 0) continue;
                 uint32_t pos = incl - cnt;
                 for (uint32_t y = word; y; y &= y - 1) sit[pos++] = wi * 32u + (uint32_t)(__ffs(y) - 1);
-                if (QUEUE && last && word) x.bm_prev[wi] = 0u;   // recycle the claim bitmap
                 __syncwarp();
                 uint32_t u1 = lane < total ? sit[lane] : NONE, pay1, beg1, end1;
                 item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
@@ -1099,6 +1105,9 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                 if (QUEUE && last && u != NONE) x.bm_prev[u >> 5] = 0u;   // recycle the claim bitmap
                 if (u != NONE && first) acc.nv++;
                 if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
+                if (ALGO == SSSP && a.skip_now && deg &&
+                    (((COHERENT ? __ldcg(x.bm_now + (u >> 5)) : x.bm_now[u >> 5]) >> (u & 31)) & 1u))
+                    deg = 0;   // queued again already: expanded next round with its newer value
                 if (STYLE == DELTA && u != NONE && pay >= x.thr) {   // bucket was split: back to the far set
                     if (first) park_far(a, x, u, pay);
                     deg = 0;

@@ -62,17 +62,20 @@ for algo in a.algos.split(","):
         if style == "delta" and algo != "sssp":
             continue
         ms = {v: [] for v in vals}
+        work = {}
         ref = None
         for r in range(a.reps + 1):   # rep 0: warm-up (layouts, CUDA graph capture)
             for v in vals:
                 st = fb.run(hs[v], algo, style, out, G.source)
                 if r:
                     ms[v].append(st.ms)
+                    work[v] = (st.iterations, st.edges_relaxed / max(G.m, 1))
                 res = out.cpu().numpy().copy()
                 if ref is None:
                     ref = res
                 assert np.array_equal(res, ref), f"{algo}/{style}: {name}={v} changed the result"
-        line = "  ".join(f"{name}={v}: {statistics.median(ms[v]):8.3f}" for v in vals)
+        line = "  ".join(f"{name}={v}: {statistics.median(ms[v]):8.3f} ({work[v][0]} rnd, {work[v][1]:.2f} m)"
+                         for v in vals)
         print(f"{a.config:10s} {algo:4s} {style:8s} {line}  ms (median of {a.reps})", flush=True)
 for v in vals:
     fb.graph_free(hs[v])
