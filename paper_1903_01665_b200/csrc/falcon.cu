@@ -935,6 +935,7 @@ falcon_status_t run_finish(falcon_graph *g, falcon_stats_t *stats) {
     }
     if (c.status == ST_NOT_CONVERGED)
         return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", g->pend_cap);
+    if (c.status == ST_QUEUE) return fail(FALCON_ERR_CUDA, "internal error: frontier queue bound exceeded");
     if (algo == SSSP && c.cand_ovf) {   // some candidate reached INF: is a reachable vertex left at INF? (R3)
         bool bad = false;
         falcon_status_t st = overflow_certificate(g, g->row_off, g->col, g->val, &bad);

@@ -40,7 +40,7 @@ enum Style : int { VERTEX = 0, EDGE = 1, WORKLIST = 2, DELTA = 3,
                    VFUSED = 4 /* partitioned VERTEX rounds writing remote targets into their owners (partition.cuh) */ };
 __host__ __device__ constexpr bool is_vertex(int style) { return style == VERTEX || style == VFUSED; }
 enum DeltaMode : uint32_t { MODE_NEAR = 0, MODE_SCAN = 1 };
-enum DevStatus : int { ST_OK = 0, ST_OVERFLOW = 5, ST_NOT_CONVERGED = 6 };
+enum DevStatus : int { ST_OK = 0, ST_OVERFLOW = 5, ST_NOT_CONVERGED = 6, ST_QUEUE = 7 /* internal: queue bound */ };
 
 // Device-resident control block: the convergence decision lives here, so no
 // host round trip happens per round (replaces the per-iteration `changed`
@@ -206,6 +206,15 @@ __device__ __forceinline__ int32_t ld_val(const int32_t *p, uint64_t pol) {
 __device__ __forceinline__ uint32_t ld_ro(const uint32_t *p) { return __ldg(p); }
 
 __device__ __forceinline__ bool bit_test(const uint32_t *bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
+
+// Frontier-queue append (fr0 / fr1 hold n + 1 entries).  Claims make every
+// round's appends distinct, so the bound is never reached; an append past it
+// is dropped and flagged (ST_QUEUE: the call fails with FALCON_ERR_CUDA and
+// no kernel writes outside the queue).
+__device__ __forceinline__ void q_put(const Args &a, uint32_t *out, uint32_t idx, uint32_t v) {
+    if (idx <= a.n) out[idx] = v;
+    else a.ctrl->status = ST_QUEUE;
+}
 
 // BFS level L of vertex v (PAPER.md:1309 `t.dist = lev+1`).  Levels below 255
 // go to a byte array (n bytes: L2-resident at 25M vertices, where the int32
@@ -418,7 +427,7 @@ __device__ __forceinline__ void scan_far_round(const Args &a, Ctrl *c, uint32_t 
         if (mv) {
             a.vis[wi] = fw & ~mv;
             atomicOr(bm_now + wi, mv);   // these are the near queue of the next round
-            for (uint32_t x = mv; x; x &= x - 1) out[b++] = wi * 32u + (uint32_t)(__ffs(x) - 1);
+            for (uint32_t x = mv; x; x &= x - 1) q_put(a, out, b++, wi * 32u + (uint32_t)(__ffs(x) - 1));
         }
         nv += cnt;
     }
@@ -683,7 +692,7 @@ constexpr uint32_t HMAX = 64;   // long rows per CTA and round (more: the warp e
 // Local continuation (LOCAL rounds): hand the warp's unexpanded local items
 // wq[qh, qn) over to the next round -- claim each in this round's bitmap and
 // append the newly claimed ones to the queue.
-__device__ __forceinline__ void spill_local(Xw &x) {
+__device__ __forceinline__ void spill_local(const Args &a, Xw &x) {
     const int lane = threadIdx.x & 31;
     for (uint32_t i0 = x.qh; i0 < x.qn; i0 += 32) {   // warp-uniform
         const uint32_t i = i0 + lane;
@@ -698,7 +707,7 @@ __device__ __forceinline__ void spill_local(Xw &x) {
         uint32_t b = 0;
         if (lane == 0) b = atomicAdd(&x.c->out_len, (uint32_t)__popc(mask));
         b = __shfl_sync(FULL, b, 0);
-        if (want) x.out[b + __popc(mask & ((1u << lane) - 1u))] = v;
+        if (want) q_put(a, x.out, b + __popc(mask & ((1u << lane) - 1u)), v);
     }
     __syncwarp();
     x.qh = x.qn = 0;
@@ -859,7 +868,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
                 }
                 x.qh = 0; x.qn = cnt;
             } else {
-                spill_local(x);
+                spill_local(a, x);
             }
         }
     } else {
@@ -888,7 +897,7 @@ __device__ __forceinline__ void relax_step(const Args &a, Xw &x, const Step<U> &
             uint32_t b = 0;
             if (lane == 0) b = atomicAdd(&x.c->out_len, x.qn);
             b = __shfl_sync(FULL, b, 0);
-            for (uint32_t i = lane; i < x.qn; i += 32) x.out[b + i] = x.wq[i];
+            for (uint32_t i = lane; i < x.qn; i += 32) q_put(a, x.out, b + i, x.wq[i]);
             __syncwarp();
             x.qn = 0;
         }
@@ -1144,7 +1153,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
             if (pend.live) relax_step<ALGO, STYLE, U, true, NOQ, LOCAL>(a, x, pend, acc);
             pend.live = false;
         }
-        spill_local(x);
+        spill_local(a, x);
     }
     if (QUEUE && !NOQ && !LOCAL) {
         __syncwarp();
@@ -1152,7 +1161,7 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
             uint32_t b = 0;
             if (lane == 0) b = atomicAdd(&c->out_len, x.qn);
             b = __shfl_sync(FULL, b, 0);
-            for (uint32_t i = lane; i < x.qn; i += 32) out[b + i] = wq[i];
+            for (uint32_t i = lane; i < x.qn; i += 32) q_put(a, out, b + i, wq[i]);
             __syncwarp();
         }
     }
@@ -1478,6 +1487,7 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
                                              uint32_t lazy_div = 0) {
     const uint32_t pull_div = aux_div;
     if (c->done) return false;
+    if (c->status == ST_QUEUE) { c->done = 1; return false; }
     c->launches += launches_per_round;
     bool more = STYLE == WORKLIST ? (c->noq ? c->changed != 0 : c->out_len > 0) : c->changed != 0;
     if (STYLE == DELTA) {

@@ -896,6 +896,8 @@ falcon_status_t run_partitioned(falcon_graph *g, int algo, uint32_t source, int3
     }
     for (auto &c : hc)
         if (c.status == ST_NOT_CONVERGED) return fail(FALCON_ERR_NOT_CONVERGED, "no fixpoint within %u rounds", cap);
+    for (auto &c : hc)
+        if (c.status == ST_QUEUE) return fail(FALCON_ERR_CUDA, "internal error: frontier queue bound exceeded");
     if (overflow) return fail(FALCON_ERR_OVERFLOW, "a finite shortest distance is >= FALCON_INF");
     g_last_error.clear();
     return FALCON_OK;
