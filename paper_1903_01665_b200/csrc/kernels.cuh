@@ -470,7 +470,7 @@ __global__ void k_sum_weights(uint64_t m, const int32_t *w, unsigned long long *
 //      visited / next-frontier words are written once, with plain stores, by
 //      the lane owning the word.
 template <int B>
-__global__ void __launch_bounds__(B) k_pull(Args a) {
+__global__ void __launch_bounds__(B, 2048 / B) k_pull(Args a) {   // 8 CTAs of 256 per SM: 32 registers
     Ctrl *c = a.ctrl;
     if (c->done) return;
     if (!c->pull) {
