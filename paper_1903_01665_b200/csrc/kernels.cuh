@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(B, 2048 / B) k_pull(Args a) {   // 8 CTAs of 2
         const int lane = threadIdx.x & 31;
         uint32_t fresh = 0;   // last (lazy) round's discoveries, counted once each
         const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
-        unsigned long long nv = 0, ne = 0, nu = 0;
+        uint32_t nv = 0, ne = 0, nu = 0;   // per-thread counts (32-bit: registers)
         bool chg = false;
         for (uint32_t wi = gw; wi < a.nwords; wi += nwarps) {
             const uint32_t prevw = bm_prev[wi];
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(B, 2048 / B) k_pull(Args a) {   // 8 CTAs of 2
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *sit = s_it[wid], *sfd = s_fd[wid];
     const uint32_t gw = (blockIdx.x * B + threadIdx.x) >> 5, nwarps = (gridDim.x * B) >> 5;
-    unsigned long long nv = 0, ne = 0, nu = 0;
+    uint32_t nv = 0, ne = 0, nu = 0;   // per-thread counts (32-bit: registers)
     bool chg = false;
     uint32_t fresh = 0;
     for (uint32_t g0 = gw * PG; g0 < a.nwords; g0 += nwarps * PG) {   // warp-uniform
