@@ -304,6 +304,9 @@ FALCON_API falcon_status_t falcon_set_delta(falcon_graph_t *g, int32_t delta);
  *   "cta_thr"      rows longer than this many arcs are expanded by the whole
  *                  CTA instead of one warp (default 1024, env FALCON_CTA_THR;
  *                  0 = warp-level only)
+ *   "bfs_wl_pull"  BFS WORKLIST rounds may run bottom-up over the in-arcs
+ *                  like VERTEX, by the same per-round cost model (default 1,
+ *                  env FALCON_BFS_WL_PULL; 0 = push only)
  *   "skip_now"     SSSP expansion styles: an item whose bit is already set in
  *                  the current round's bitmap (improved again this round, so
  *                  it is expanded next round with its newer value) is not

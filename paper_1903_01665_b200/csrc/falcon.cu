@@ -209,6 +209,8 @@ struct falcon_graph {
     uint32_t lazy_div = 256;             // BFS VERTEX lazy visited set in push rounds with frontier > n / lazy_div
                                          // (option bfs_lazy_div / FALCON_BFS_LAZY_DIV; 0 = never)
     uint32_t cta_thr = 1024;             // CTA-level expansion of rows longer than this (FALCON_CTA_THR / option cta_thr; 0 = off)
+    uint32_t wl_pull = 1;                // BFS WORKLIST: bottom-up rounds like VERTEX (FALCON_BFS_WL_PULL / option
+                                         // bfs_wl_pull; 0 = push only)
     uint32_t skip_now = 1;               // SSSP: an item already re-activated for the next round is not expanded now
                                          // (FALCON_SKIP_NOW / option skip_now; 0 = off)
     uint32_t pull_rule = 0;              // BFS VERTEX direction: 0 cost model; 1 / 2 pull iff frontier > n / pull_div,
@@ -298,6 +300,7 @@ struct falcon_graph {
         a.dl_noq = dl_noq;
         a.cta_thr = cta_thr;
         a.skip_now = skip_now;
+        a.wl_pull = wl_pull && pull_div && !unit_run && rin_off && !persist ? 1u : 0u;
         a.local_tiles = local_tiles;
         a.local_max = local_max;
         a.wl_local_tiles = wl_local_tiles;
@@ -425,6 +428,11 @@ struct Round {
                 launches++;
                 if (tr) tr->mark(s, "persist", 0);
             }
+            if (ALGO == BFS && a.wl_pull && !g->persist) {   // bottom-up rounds
+                launch_l2(g, k_pull<BLOCK>, g->grid_pull, s, a);
+                launches++;
+                if (tr) tr->mark(s, "pull", 0);
+            }
             launch_expand_warp<ALGO, WORKLIST>(g, s, a);
             if (tr) tr->mark(s, "expand", 0);
         } else {
@@ -435,7 +443,9 @@ struct Round {
         launches++;
         launches++;
         k_advance<ALGO, STYLE><<<1, 32, 0, s>>>(g->ctrl, h, in_graph, (uint32_t)launches, (uint32_t)g->n,
-                                                 STYLE == DELTA ? g->split_div : g->pull_div, g->blk_div, g->pull_rule,
+                                                 STYLE == DELTA ? g->split_div
+                                                 : (STYLE == WORKLIST && !a.wl_pull ? 0u : g->pull_div),
+                                                 g->blk_div, g->pull_rule,
                                                  (uint32_t)g->m, g->lazy_div);
         if (tr) tr->mark(s, "advance", 1);
         return launches;
@@ -744,7 +754,8 @@ falcon_status_t run_launch(falcon_graph *g, int algo, uint32_t source, int style
             falcon_status_t st = ensure_blocked(g);
             if (st != FALCON_OK) return st;
         }
-        if ((algo == BFS && style == VERTEX && g->pull_div) || (algo == CC && style == WORKLIST)) {
+        if ((algo == BFS && (style == VERTEX || (style == WORKLIST && g->wl_pull && !unit)) && g->pull_div) ||
+            (algo == CC && style == WORKLIST)) {
             falcon_status_t st = ensure_reverse(g);
             if (st != FALCON_OK) return st;
         }
@@ -1161,6 +1172,7 @@ falcon_status_t load(int64_t n, int64_t m, const uint32_t *row_off, const uint32
     if (const char *pu = getenv("FALCON_BFS_PULL_RULE")) g->pull_rule = (uint32_t)atoi(pu);
     if (const char *ct = getenv("FALCON_CTA_THR")) g->cta_thr = (uint32_t)atoi(ct);
     if (const char *sn = getenv("FALCON_SKIP_NOW")) g->skip_now = (uint32_t)atoi(sn);
+    if (const char *wp = getenv("FALCON_BFS_WL_PULL")) g->wl_pull = (uint32_t)atoi(wp);
     if (const char *lv = getenv("FALCON_BFS_LAZY_DIV")) g->lazy_div = (uint32_t)atoi(lv);
     int slots = g->grid_persist;
     for (int gsz : {g->grid_expand_fr, g->grid_expand_dl, g->grid_edge, g->grid_edge_b, g->grid_small, g->grid_cc,
@@ -1239,7 +1251,7 @@ falcon_status_t share(falcon_graph *p, const falcon_load_opts_t *opts, falcon_gr
     v->wl_local_tiles = p->wl_local_tiles; v->wl_local_max = p->wl_local_max; v->delta_cap = p->delta_cap;
     v->bfs_unit = p->bfs_unit;
     v->rin_off = p->rin_off; v->rin_col = p->rin_col; v->pull_div = p->pull_div; v->pull_rule = p->pull_rule; v->cta_thr = p->cta_thr; v->lazy_div = p->lazy_div;
-    v->skip_now = p->skip_now;
+    v->skip_now = p->skip_now; v->wl_pull = p->wl_pull;
     v->nwords = p->nwords; v->num_sms = p->num_sms;
     v->grid_persist = p->grid_persist; v->grid_expand_fr = p->grid_expand_fr; v->grid_expand_dl = p->grid_expand_dl;
     v->grid_pull = p->grid_pull; v->grid_cc = p->grid_cc; v->grid_edge = p->grid_edge; v->grid_edge_b = p->grid_edge_b;
@@ -1548,6 +1560,8 @@ falcon_status_t falcon_set_option(falcon_graph_t *g, const char *name, int64_t v
             t->cta_thr = (uint32_t)value;
         } else if (!strcmp(name, "skip_now")) {
             t->skip_now = (uint32_t)value;
+        } else if (!strcmp(name, "bfs_wl_pull")) {
+            t->wl_pull = (uint32_t)value;
         } else if (!strcmp(name, "pull_rule")) {
             t->pull_rule = (uint32_t)value;
         } else if (!strcmp(name, "persist")) {

@@ -110,6 +110,7 @@ struct Args {
     uint32_t wl_noq;           // WORKLIST dense rounds mark like VERTEX (no claim / queue); 0 = off
     uint32_t dl_noq;           // ... DELTA dense rounds (near marks in the bitmap, far parking as usual)
     uint32_t cta_thr;          // rows longer than this are expanded by the whole CTA (0: warp-level only)
+    uint32_t wl_pull;          // BFS WORKLIST: rounds may run bottom-up (k_pull) like VERTEX (0: push only)
     uint32_t skip_now;         // SSSP: an item whose bit is already set in this round's bitmap (improved again
                                // this round, so expanded next round with its newer value) is not expanded now
     uint32_t lazy_div;         // BFS VERTEX: a push round whose frontier exceeds n / lazy_div marks only the
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(B, 2048 / B) k_pull(Args a) {   // 8 CTAs of 2
     }
     const uint32_t iter = c->iter, lev = iter - 1;
     clear_next_bitmap(a, iter);
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->noq = 1;   // WORKLIST: the next round reads its items from bm_now
     const uint32_t *bm_prev = bm_of(a, iter - 1);
     uint32_t *bm_now = bm_of(a, iter);
     const bool merge = c->merge != 0;   // (vis lacks last round's discoveries: visw |= prevw below, written back)
@@ -1086,7 +1088,8 @@ __device__ __forceinline__ void expand_round(const Args &a, Ctrl *c, uint32_t it
                     item_rows<ALGO, COHERENT>(a, x, u1, pay1, beg1, end1);
                     if (u != NONE && first) {
                         acc.nv++;
-                        if (ALGO == BFS && is_vertex(STYLE)) put_level(a, u, x.lev);   // discovered last round
+                        if (ALGO == BFS && (is_vertex(STYLE) || (STYLE == WORKLIST && a.wl_pull)))
+                            put_level(a, u, x.lev);   // discovered last round (WORKLIST: maybe by a pull round)
                     }
                     if (u == NONE || (ALGO == SSSP && pay == (uint32_t)INF)) deg = 0;
                     if (STYLE == DELTA && u != NONE && pay >= x.thr) {   // bucket was split: back to the far set
@@ -1192,7 +1195,7 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
     static_assert(is_vertex(STYLE) || STYLE == WORKLIST || STYLE == DELTA, "expand is for VERTEX/WORKLIST/DELTA");
     constexpr int WQ = (STYLE == WORKLIST || STYLE == DELTA) ? 256 : 1;
     Ctrl *c = a.ctrl;
-    if (c->done || (ALGO == BFS && is_vertex(STYLE) && c->pull)) return;
+    if (c->done || (ALGO == BFS && (is_vertex(STYLE) || STYLE == WORKLIST) && c->pull)) return;
     if (STYLE == DELTA && c->mode != MODE_NEAR) {   // this round refills the near queue from the far set
         unsigned long long nv = 0;
         scan_far_round<false>(a, c, c->iter, c->thr, c->sel ? a.fr0 : a.fr1, nv);
@@ -1200,7 +1203,9 @@ __global__ void __launch_bounds__(B, MINB) k_expand_warp(Args a) {
         return;
     }
     const uint32_t iter = c->iter;
-    if (is_vertex(STYLE)) clear_next_bitmap(a, iter);
+    // (BFS WORKLIST with pull rounds: a pull round leaves its input bitmap
+    // unrecycled, so every round clears the one after next like VERTEX)
+    if (is_vertex(STYLE) || (ALGO == BFS && STYLE == WORKLIST && a.wl_pull)) clear_next_bitmap(a, iter);
     const uint32_t thr = STYLE == DELTA ? c->thr : 0xffffffffu;
     const uint32_t *in = c->sel ? a.fr1 : a.fr0;
     uint32_t *out = c->sel ? a.fr0 : a.fr1;
@@ -1548,6 +1553,13 @@ __device__ __forceinline__ bool advance_step(Ctrl *c, uint32_t launches_per_roun
             // after a no-queue round the frontier size is estimated by the
             // filter passes (>= the improved vertices): it only decides dense
             c->in_len = STYLE == WORKLIST && c->noq ? c->found : c->out_len;
+            if (ALGO == BFS && STYLE == WORKLIST && pull_div) {   // bottom-up rounds (option wl_pull)
+                c->visited += c->noq ? c->found : c->out_len;   // (no-queue rounds: marks, an over-count)
+                c->found = c->noq ? c->found : c->out_len;
+                c->pull = bfs_direction(c, n, m, pull_div, rule);
+                c->rnd_items = 0;
+                c->rnd_edges = 0;
+            }
             c->prevnoq = c->noq;
             c->noq = 0;
             c->out_len = 0;
@@ -1614,7 +1626,7 @@ __device__ __forceinline__ void grid_barrier_advance(Ctrl *c, uint32_t n, uint32
         const uint32_t arrived = atomicAdd(&c->bar_arrive, 1u);
         if (arrived == gridDim.x - 1) {
             c->bar_arrive = 0;
-            advance_step<ALGO, STYLE>(c, 0u, n, pull_div, blk_div);
+            advance_step<ALGO, STYLE>(c, 0u, n, STYLE == WORKLIST && ALGO == BFS ? 0u : pull_div, blk_div);   // (no bottom-up rounds here)
             __threadfence();
             atomicExch(&c->bar_gen, gen + 1u);
         } else {
