@@ -21,7 +21,7 @@ import paper_1903_01665_b200 as fb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--jobs", required=True)
 ap.add_argument("--iters", type=int, default=300)
-ap.add_argument("--views", type=int, default=1)
+ap.add_argument("--views", type=int, default=1, help="1: graph_share views, 2: independent loads, 0: sequential")
 ap.add_argument("--config", default="rand-s")
 ap.add_argument("--profile", type=int, default=0, help="host-driven rounds (no CUDA graphs / conditional nodes)")
 a = ap.parse_args()
@@ -31,7 +31,10 @@ exp = {al: oracle.run(al, G) for al in {j[0] for j in jobs}}
 for it in range(a.iters):
     try:
         g = fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0)
-        hs = [g] + ([fb.graph_share(g) for _ in range(len(jobs) - 1)] if a.views else [])
+        if a.views == 2:   # independent loads: no arrays shared between the handles
+            hs = [g] + [fb.graph_load_csr(G.n, G.m, G.row_off, G.col, G.w, device=0) for _ in range(len(jobs) - 1)]
+        else:
+            hs = [g] + ([fb.graph_share(g) for _ in range(len(jobs) - 1)] if a.views else [])
         if a.profile:
             for h in hs:
                 fb.falcon_set_profiling(h, True)
